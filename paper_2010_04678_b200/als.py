@@ -1,0 +1,141 @@
+"""Single-instance ALS mathematics (API of the reference's ``cals.als``).
+
+``update_factor`` runs the batched update kernel (csrc/update.cuh) for one
+block on the GPU; ``run_single_als`` is the device-resident driver at K=1.
+``fast_error`` / ``fit_from_error`` are the scalar formulas the engine
+evaluates on the device (exposed for callers that hold host arrays).
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import math
+from dataclasses import dataclass
+from typing import Sequence
+
+import numpy as np
+
+from . import _native
+from .tensor import hadamard_fold
+
+
+@dataclass
+class ConvergenceConfig:
+    """Stop when the fit improves by less than ``tol`` or after
+    ``max_iterations``; ``tol <= 0`` disables the fit test (als.py:24-37)."""
+
+    tol: float = 1e-6
+    max_iterations: int = 1000
+
+    def __post_init__(self):
+        if self.max_iterations < 1:
+            raise ValueError("max_iterations must be >= 1")
+
+
+@dataclass
+class LineSearchConfig:
+    """Linear extrapolation between iterates (als.py:40-53); ``alpha=None``
+    selects alpha = i^(1/3)."""
+
+    enabled: bool = False
+    alpha: float | None = None
+
+    def __post_init__(self):
+        if self.alpha is not None and self.alpha <= 1.0:
+            raise ValueError(f"extrapolation alpha must be > 1, got {self.alpha}")
+
+
+def alpha_for_iteration(cfg: LineSearchConfig, iteration: int) -> float:
+    return cfg.alpha if cfg.alpha is not None else float(iteration) ** (1.0 / 3.0)
+
+
+class NnlsState:
+    """Per-mode, per-row active sets (True = pinned to zero)."""
+
+    def __init__(self, dims: Sequence[int], rank: int):
+        self.active = [np.zeros((int(d), rank), dtype=bool) for d in dims]
+
+
+class NonConvergedNnlsWarning(RuntimeWarning):
+    """Active-set search hit its iteration cap."""
+
+
+def update_factor(m: np.ndarray, h: np.ndarray) -> np.ndarray:
+    """Solve ``A @ h = m`` on the GPU (replaces als.py:74-96): upper Cholesky
+    + triangular solves, eigen-pinv fallback (cutoff 1e-12 * lambda_max).
+    Raises ValueError for a non-square ``h`` or non-finite inputs."""
+    import torch
+
+    m = np.asarray(m, dtype=np.float64)
+    h = np.asarray(h, dtype=np.float64)
+    if h.ndim != 2 or h.shape[0] != h.shape[1]:
+        raise ValueError(f"h must be square, got {h.shape}")
+    if m.ndim != 2 or m.shape[1] != h.shape[0]:
+        raise ValueError(f"m has shape {m.shape}, expected (*, {h.shape[0]})")
+    rows, r = m.shape
+    if r > 128:
+        raise ValueError("update_factor supports rank <= 128 on the GPU")
+    lib = _native.load()
+    dev = torch.device("cuda", torch.cuda.current_device())
+    md = torch.from_numpy(np.ascontiguousarray(m)).to(dev)
+    hd = torch.from_numpy(np.ascontiguousarray(h)).to(dev)
+    ad = torch.empty((max(rows, 1), r), dtype=torch.float64, device=dev)
+    scratch = torch.empty((lib.cals_update_scratch_bytes(r) + 7) // 8, dtype=torch.float64,
+                          device=dev)
+    status = torch.zeros(1, dtype=torch.int32, device=dev)
+    _native.call("cals_update_factor", rows, r, md.data_ptr(), r, hd.data_ptr(), ad.data_ptr(), r,
+                 scratch.data_ptr(), status.data_ptr(), torch.cuda.current_stream().cuda_stream)
+    if int(status.item()) != 0:
+        raise ValueError("non-finite input to factor update")
+    return np.asfortranarray(ad[:rows].cpu().numpy())
+
+
+def fast_error(t_sqnorm: float, factors: Sequence[np.ndarray], last_mttkrp: np.ndarray,
+               grams: Sequence[np.ndarray]) -> float:
+    """||T||^2 + sum(hadamard of all Gramians) - 2 <A_last, M_last>, clamped
+    with ``e if e > 0 else 0`` (als.py:99-115; NaN clamps to 0 as there)."""
+    e = (t_sqnorm + float(hadamard_fold(grams).sum())
+         - 2.0 * float(np.vdot(np.asarray(factors[-1]), np.asarray(last_mttkrp))))
+    return e if e > 0.0 else 0.0
+
+
+def fit_from_error(e: float, t_sqnorm: float) -> float:
+    """1 - sqrt(e)/||T|| (als.py:118-124)."""
+    if t_sqnorm <= 0.0:
+        raise ValueError("tensor squared norm must be positive")
+    if e < 0.0:
+        raise ValueError(f"negative squared error {e}")
+    return 1.0 - math.sqrt(e) / math.sqrt(t_sqnorm)
+
+
+_NEXT = ("line search and non-negative updates are the next rows of the hot-path "
+         "scope (SURVEY.md section 8f) and are not implemented on the GPU yet")
+
+
+def extrapolate_factors(*args, **kwargs):
+    raise NotImplementedError(_NEXT)
+
+
+def line_search_step(*args, **kwargs):
+    raise NotImplementedError(_NEXT)
+
+
+def nnls_solve_row(*args, **kwargs):
+    raise NotImplementedError(_NEXT)
+
+
+def nnls_update(*args, **kwargs):
+    raise NotImplementedError(_NEXT)
+
+
+def run_single_als(t, start, cfg: ConvergenceConfig, ls: LineSearchConfig | None = None,
+                   nonneg: bool = False, ws=None, variant_table=None):
+    """Fit one instance (als.py:281-356) -- the device-resident driver at K=1,
+    which is bitwise identical to that model's columns in a fused run."""
+    from .driver import ExecutionMode, run
+
+    if start.dims != t.dims:
+        raise ValueError(f"model dims {start.dims} != tensor dims {t.dims}")
+    (out,) = run(t, [start], cfg, mode=ExecutionMode.CALS, r_star=start.rank, ls=ls,
+                 nonneg=nonneg, variant_table=variant_table)
+    return out

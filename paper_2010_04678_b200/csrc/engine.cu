@@ -1,0 +1,898 @@
+// Device-resident CALS driver (Algorithm 4 of arXiv 2010.04678).
+//
+// Restates pkg/src/cals/driver.py:185-307 (`_run_cals`) with every piece of
+// per-iteration state in HBM:
+//   * factor multi-matrices, one row-major [I_n][ld] buffer per mode (the
+//     reference keeps Fortran (I_n, R*) buffers, multimatrix.py:33-120);
+//   * per-model Gramians, status, iteration count, f_prev, error, fit;
+//   * the slot layout (registry order) and the FIFO admission queue.
+// One driver iteration is a fixed kernel sequence captured once in a CUDA
+// graph:  for n in modes: [fused MTTKRP(n) -> split reduce -> update(n)]
+// (fit fused into update(N-1)), then plan (retire / compact / admit, trace)
+// and move (retire copy-out, compaction, admission copy-in).  The host only
+// replays the graph and polls a mapped "done" flag; no per-iteration host
+// round trip.
+#include <algorithm>
+#include <chrono>
+#include <cstring>
+#include <numeric>
+#include <vector>
+
+#include "internal.h"
+#include "mttkrp.cuh"
+#include "update.cuh"
+
+namespace cals {
+
+enum Status : int { kPending = 0, kActive = 1, kConverged = 2, kCap = 3, kFailed = 4 };
+enum MoveKind : int { kMoveKeep = 0, kMoveRetire = 1, kMoveAdmit = 2 };
+
+struct EngState {
+  // scalars
+  int order, n_models, capacity, max_slots;
+  int width, n_active, queue_head, n_retired;
+  int plans_done;   // number of plan() calls that did work (trace records)
+  int done;
+  int old_width, n_moves, move_elems;
+  int max_rank;
+  double tol, sqnorm;
+  int max_iterations;
+  long long ld;
+  long long dims[kMaxOrder];
+  // slots
+  int* slot_model;
+  int* slot_off;
+  // move plan
+  int* mv_kind;
+  int* mv_model;
+  int* mv_src;
+  int* mv_dst;
+  int* mv_len;
+  int* mv_pre;  // exclusive prefix of lengths
+  // per model (const)
+  const int* rank;
+  const long long* pool_off;  // [k * order + n]
+  const long long* gram_off;  // [k]
+  long long gram_stride;
+  // per model (state)
+  int* status;
+  int* iters;
+  int* failed;
+  int* fresh;
+  int* retire_seq;
+  double* f_prev;
+  double* err;
+  double* fit;
+  unsigned long long* t_admit;
+  unsigned long long* t_retire;
+  double* grams;  // [order][gram_stride]
+  double* pool;
+  double* F[kMaxOrder];
+  double* Mout;
+  double* scratch;  // per-block pinv scratch
+  // trace
+  int tr_cap;
+  int* tr_width;
+  int* tr_active;
+  unsigned long long* tr_time;
+  volatile int* host_done;
+};
+
+// ------------------------------------------------------------------ update --
+__global__ void __launch_bounds__(kUpdThreads) engine_update_kernel(EngState* st, int n,
+                                                                     int nthr) {
+  extern __shared__ __align__(16) double dsm[];
+  __shared__ int flag;
+  __shared__ double red[kUpdThreads];
+  const int N = st->order;
+  const int Rmax = st->max_rank;
+  double* H = dsm;                // Rmax^2
+  double* X = H + Rmax * Rmax;    // Rmax * nthr
+  double* V = st->scratch + (long long)blockIdx.x * (2 * Rmax * Rmax + Rmax);
+  double* Hsave = V + Rmax * Rmax;
+  double* lam = Hsave + Rmax * Rmax;
+  const int rows = (int)st->dims[n];
+  const long long ld = st->ld;
+  const int n_active = st->n_active;
+
+  for (int slot = blockIdx.x; slot < n_active; slot += gridDim.x) {
+    const int k = st->slot_model[slot];
+    const int R = st->rank[k];
+    const int off = st->slot_off[slot];
+    const long long go = st->gram_off[k];
+    auto gram = [&](int i) { return st->grams + i * st->gram_stride + go; };
+
+    if (n == 0 && st->fresh[k]) {
+      // Gramians of the admitted starting point (driver.py:203-205)
+      for (int i = 1; i < N; ++i) block_gram(st->F[i], ld, off, (int)st->dims[i], R, gram(i));
+      __syncthreads();
+      if (threadIdx.x == 0) st->fresh[k] = 0;
+    }
+    bool updated = false;
+    if (!st->failed[k]) {
+      for (int idx = threadIdx.x; idx < R * R; idx += blockDim.x) {
+        double h = 1.0;
+        bool first = true;
+        for (int i = 0; i < N; ++i) {
+          if (i == n) continue;
+          const double g = gram(i)[idx];
+          h = first ? g : h * g;
+          first = false;
+        }
+        H[idx] = h;
+      }
+      __syncthreads();
+      const bool finite_in = block_update(H, Hsave, V, lam, X, nthr, R, st->Mout + off, ld, rows,
+                                          st->F[n] + off, ld, &flag);
+      if (!finite_in) {
+        if (threadIdx.x == 0) st->failed[k] = 1;
+      } else {
+        block_gram(st->F[n], ld, off, rows, R, gram(n));
+        updated = true;
+      }
+      __syncthreads();
+    }
+    if (n == N - 1) {
+      // fast error / fit / stopping rule (driver.py:241-273, als.py:99-124)
+      double inner = 0.0, msq = 0.0;
+      if (updated) {
+        double part = 0.0;
+        for (long long e = threadIdx.x; e < (long long)rows * R; e += blockDim.x) {
+          const long long i = e / R;
+          const int r = int(e % R);
+          part = fma(st->F[n][i * ld + off + r], st->Mout[i * ld + off + r], part);
+        }
+        inner = block_sum(part, red);
+        double mpart = 0.0;
+        for (int idx = threadIdx.x; idx < R * R; idx += blockDim.x) {
+          double h = gram(0)[idx];
+          for (int i = 1; i < N; ++i) h *= gram(i)[idx];
+          mpart += h;
+        }
+        msq = block_sum(mpart, red);
+      }
+      if (threadIdx.x == 0) {
+        const int it = ++st->iters[k];
+        if (st->failed[k]) {
+          st->err[k] = nan("");
+          st->fit[k] = -INFINITY;
+          st->status[k] = kFailed;
+        } else {
+          double e = st->sqnorm + msq - 2.0 * inner;
+          e = e > 0.0 ? e : 0.0;
+          if (!isfinite(e)) {
+            st->err[k] = e;
+            st->fit[k] = -INFINITY;
+            st->status[k] = kFailed;
+          } else {
+            const double f = 1.0 - sqrt(e) / sqrt(st->sqnorm);
+            st->err[k] = e;
+            st->fit[k] = f;
+            if (st->tol > 0.0 && f - st->f_prev[k] < st->tol)
+              st->status[k] = kConverged;
+            else if (it >= st->max_iterations)
+              st->status[k] = kCap;
+            else
+              st->f_prev[k] = f;
+          }
+        }
+      }
+      __syncthreads();
+    }
+  }
+}
+
+// -------------------------------------------------------------------- plan --
+// One warp: retire (registry order), compact survivors, admit FIFO with
+// head-of-line blocking (driver.py:198-208, 274-276; multimatrix.py:103-158).
+__global__ void engine_plan_kernel(EngState* st) {
+  if (st->done) return;
+  const int lane = threadIdx.x;
+  const unsigned long long now = globaltimer_ns();
+  const int n_old = st->n_active;
+  int new_n = 0, new_w = 0, retired = st->n_retired, moves = 0;
+  for (int base = 0; base < n_old; base += 32) {
+    const int s = base + lane;
+    const bool valid = s < n_old;
+    const int k = valid ? st->slot_model[s] : 0;
+    const bool retiring = valid && st->status[k] != kActive;
+    const bool keep = valid && !retiring;
+    const int rk = keep ? st->rank[k] : 0;
+    int incl = rk;
+    for (int o = 1; o < 32; o <<= 1) {
+      const int v = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += v;
+    }
+    const unsigned rmask = __ballot_sync(0xffffffffu, retiring);
+    const unsigned kmask = __ballot_sync(0xffffffffu, keep);
+    const unsigned below = (1u << lane) - 1u;
+    const int src = valid ? st->slot_off[s] : 0;
+    if (retiring) {
+      const int seq = retired + __popc(rmask & below);
+      st->retire_seq[k] = seq;
+      st->t_retire[k] = now;
+      const int mi = moves + __popc((rmask | kmask) & below);
+      st->mv_kind[mi] = kMoveRetire;
+      st->mv_model[mi] = k;
+      st->mv_src[mi] = src;
+      st->mv_dst[mi] = 0;
+      st->mv_len[mi] = st->rank[k];
+    }
+    if (keep) {
+      const int dst = new_w + incl - rk;
+      const int ns = new_n + __popc(kmask & below);
+      // slot arrays are compacted in place: ns <= s and every read of slot s
+      // in this warp happened above
+      const int mi = moves + __popc((rmask | kmask) & below);
+      st->mv_kind[mi] = kMoveKeep;
+      st->mv_model[mi] = k;
+      st->mv_src[mi] = src;
+      st->mv_dst[mi] = dst;
+      st->mv_len[mi] = dst != src ? rk : 0;
+      __syncwarp(kmask);
+      st->slot_model[ns] = k;
+      st->slot_off[ns] = dst;
+    }
+    __syncwarp();
+    new_w += __shfl_sync(0xffffffffu, incl, 31);
+    new_n += __popc(kmask);
+    retired += __popc(rmask);
+    moves += __popc(rmask | kmask);
+  }
+  if (lane == 0) {
+    int head = st->queue_head;
+    while (head < st->n_models && new_w + st->rank[head] <= st->capacity) {
+      const int k = head++;
+      st->status[k] = kActive;
+      st->fresh[k] = 1;
+      st->t_admit[k] = now;
+      st->slot_model[new_n] = k;
+      st->slot_off[new_n] = new_w;
+      st->mv_kind[moves] = kMoveAdmit;
+      st->mv_model[moves] = k;
+      st->mv_src[moves] = 0;
+      st->mv_dst[moves] = new_w;
+      st->mv_len[moves] = st->rank[k];
+      ++moves;
+      ++new_n;
+      new_w += st->rank[k];
+    }
+    int pre = 0;
+    for (int i = 0; i < moves; ++i) {
+      st->mv_pre[i] = pre;
+      pre += st->mv_len[i];
+    }
+    st->old_width = st->width;
+    st->move_elems = pre;
+    st->n_moves = moves;
+    st->queue_head = head;
+    st->n_active = new_n;
+    st->width = new_w;
+    st->n_retired = retired;
+    const int rec = st->plans_done;
+    if (rec < st->tr_cap) {
+      st->tr_width[rec] = new_w;
+      st->tr_active[rec] = new_n;
+      st->tr_time[rec] = now;
+    }
+    st->plans_done = rec + 1;
+    if (new_n == 0 && head >= st->n_models) {
+      st->done = 1;
+      *st->host_done = 1;
+      __threadfence_system();
+    }
+  }
+}
+
+// -------------------------------------------------------------------- move --
+// One block per (mode, row): snapshot the old active row, then apply the move
+// list -> no in-place hazards.
+__global__ void engine_move_kernel(EngState* st) {
+  const int total = st->move_elems;
+  if (total == 0) return;
+  extern __shared__ __align__(16) double row[];
+  const int N = st->order;
+  long long rows_total = 0;
+  for (int n = 0; n < N; ++n) rows_total += st->dims[n];
+  const int ow = st->old_width;
+  const int nm = st->n_moves;
+  for (long long gr = blockIdx.x; gr < rows_total; gr += gridDim.x) {
+    int n = 0;
+    long long i = gr;
+    while (i >= st->dims[n]) {
+      i -= st->dims[n];
+      ++n;
+    }
+    double* F = st->F[n] + i * st->ld;
+    for (int c = threadIdx.x; c < ow; c += blockDim.x) row[c] = F[c];
+    __syncthreads();
+    for (int e = threadIdx.x; e < total; e += blockDim.x) {
+      int lo = 0, hi = nm - 1;  // last move with mv_pre <= e
+      while (lo < hi) {
+        const int mid = (lo + hi + 1) >> 1;
+        if (st->mv_pre[mid] <= e) lo = mid; else hi = mid - 1;
+      }
+      const int r = e - st->mv_pre[lo];
+      const int k = st->mv_model[lo];
+      const int R = st->rank[k];
+      const long long po = st->pool_off[(long long)k * N + n] + i * R + r;
+      switch (st->mv_kind[lo]) {
+        case kMoveKeep: F[st->mv_dst[lo] + r] = row[st->mv_src[lo] + r]; break;
+        case kMoveRetire: st->pool[po] = row[st->mv_src[lo] + r]; break;
+        default: F[st->mv_dst[lo] + r] = st->pool[po]; break;
+      }
+    }
+    __syncthreads();
+  }
+}
+
+// ----------------------------------------------------- standalone update --
+// update_factor(m, h) for one block (als.py:74-96): rows x R, row-major.
+__global__ void __launch_bounds__(kUpdThreads) standalone_update_kernel(
+    const double* Mb, long long ldm, int rows, int R, const double* Hin, double* A, long long lda,
+    double* scratch, int nthr, int* status) {
+  extern __shared__ __align__(16) double dsm[];
+  __shared__ int flag;
+  double* H = dsm;
+  double* X = H + R * R;
+  for (int idx = threadIdx.x; idx < R * R; idx += blockDim.x) H[idx] = Hin[idx];
+  __syncthreads();
+  const bool ok = block_update(H, scratch + R * R, scratch, scratch + 2 * R * R, X, nthr, R, Mb,
+                               ldm, rows, A, lda, &flag);
+  if (threadIdx.x == 0) *status = ok ? 0 : 1;
+}
+
+// ------------------------------------------------------------------- lambdas --
+// lambda_r = prod_n ||A_n[:, r]|| of every retired model (pool layout).
+__global__ void lambdas_kernel(const EngState* st, const long long* lam_off, double* lam) {
+  const int N = st->order;
+  for (int k = blockIdx.x; k < st->n_models; k += gridDim.x) {
+    const int R = st->rank[k];
+    for (int r = threadIdx.x; r < R; r += blockDim.x) {
+      double prod = 1.0;
+      for (int n = 0; n < N; ++n) {
+        const double* P = st->pool + st->pool_off[(long long)k * N + n];
+        double s = 0.0;
+        for (long long i = 0; i < st->dims[n]; ++i) s = fma(P[i * R + r], P[i * R + r], s);
+        prod *= sqrt(s);
+      }
+      lam[lam_off[k] + r] = prod;
+    }
+  }
+}
+
+// ============================================================== host side ==
+
+static int pick_nthr(int R) {
+  int nthr = kUpdThreads;
+  while (nthr > 32 && (long long)R * nthr * 8 > 96 * 1024) nthr -= 32;
+  return nthr;
+}
+
+struct Engine {
+  Tensor* t = nullptr;
+  int order = 0, n_models = 0, capacity = 0, max_slots = 0, max_rank = 0;
+  long long ld = 0;
+  std::vector<int> ranks;
+  std::vector<long long> pool_off, gram_off, lam_off;
+  long long pool_elems = 0, gram_stride = 0, lam_elems = 0;
+  // device allocations
+  EngState* d_st = nullptr;
+  EngState h_st{};
+  void* d_block = nullptr;  // one arena for everything else
+  double* d_lam = nullptr;
+  long long* d_lam_off = nullptr;
+  size_t ws_bytes = 0;
+  double* d_ws = nullptr;
+  int* h_done = nullptr;  // mapped pinned
+  int* d_done_alias = nullptr;
+  int variants[kMaxOrder];
+  int upd_grid = 0, upd_nthr = 0;
+  size_t upd_smem = 0, move_smem = 0;
+  int move_grid = 0;
+  cudaGraph_t graph = nullptr;
+  cudaGraphExec_t exec = nullptr;
+  cudaStream_t cap_stream = nullptr;
+  int trace_cap = 0;
+  int last_iterations = 0;
+};
+
+static size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
+
+static int engine_free(Engine* e) {
+  if (!e) return kOk;
+  if (e->exec) cudaGraphExecDestroy(e->exec);
+  if (e->graph) cudaGraphDestroy(e->graph);
+  if (e->d_block) cudaFree(e->d_block);
+  if (e->d_ws) cudaFree(e->d_ws);
+  if (e->d_st) cudaFree(e->d_st);
+  if (e->h_done) cudaFreeHost(e->h_done);
+  delete e;
+  return kOk;
+}
+
+static int engine_create(Tensor* t, int capacity, int n_models, const int* ranks, int trace_cap,
+                         Engine** out) {
+  CALS_CHECK(t && out && ranks, kErrInvalid, "null argument");
+  CALS_CHECK(capacity >= 1, kErrInvalid, "capacity (r_star) must be >= 1");
+  CALS_CHECK(n_models >= 0, kErrInvalid, "n_models must be >= 0");
+  std::unique_ptr<Engine> e(new Engine());
+  e->t = t;
+  e->order = t->order;
+  e->n_models = n_models;
+  e->capacity = capacity;
+  e->ranks.assign(ranks, ranks + n_models);
+  const int N = t->order;
+  int rmax = 1;
+  long long rsum = 0;
+  for (int k = 0; k < n_models; ++k) {
+    CALS_CHECK(ranks[k] >= 1, kErrInvalid, "ranks must be >= 1");
+    CALS_CHECK(ranks[k] <= capacity, kErrCapacity,
+               "model rank " + std::to_string(ranks[k]) + " exceeds r_star " +
+                   std::to_string(capacity));
+    rmax = std::max(rmax, ranks[k]);
+    rsum += ranks[k];
+  }
+  CALS_CHECK(rmax <= 128, kErrUnsupported, "ranks above 128 are not supported by the update kernel");
+  e->max_rank = rmax;
+  e->max_slots = std::max(1, std::min<int>(n_models, capacity));
+  e->ld = align_up(capacity, 8);
+  CALS_CHECK(e->ld * 8 <= 200 * 1024, kErrUnsupported, "r_star above 25600 is not supported");
+  e->pool_off.resize((size_t)n_models * N);
+  e->gram_off.resize(n_models);
+  e->lam_off.resize(n_models);
+  long long po = 0, go = 0, lo = 0;
+  for (int k = 0; k < n_models; ++k) {
+    for (int n = 0; n < N; ++n) {
+      e->pool_off[(size_t)k * N + n] = po;
+      po += t->dims[n] * ranks[k];
+    }
+    e->gram_off[k] = go;
+    go += (long long)ranks[k] * ranks[k];
+    e->lam_off[k] = lo;
+    lo += ranks[k];
+  }
+  e->pool_elems = po;
+  e->gram_stride = std::max<long long>(go, 1);
+  e->lam_elems = std::max<long long>(lo, 1);
+  e->trace_cap = std::max(trace_cap, 1);
+
+  // launch geometry
+  const int sms = sm_count(t->device);
+  e->upd_grid = std::max(1, std::min(e->max_slots, sms * 4));
+  e->upd_nthr = pick_nthr(rmax);
+  e->upd_smem = size_t(rmax) * rmax * 8 + size_t(rmax) * e->upd_nthr * 8;
+  e->move_smem = size_t(e->ld) * 8;
+  long long rows_total = 0, maxI = 1;
+  for (int n = 0; n < N; ++n) {
+    rows_total += t->dims[n];
+    maxI = std::max(maxI, t->dims[n]);
+  }
+  e->move_grid = (int)std::max<long long>(1, std::min<long long>(rows_total, sms * 8));
+  CALS_CUDA_TRY(cudaFuncSetAttribute(engine_update_kernel,
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)e->upd_smem));
+  CALS_CUDA_TRY(cudaFuncSetAttribute(engine_move_kernel,
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)e->move_smem));
+
+  // arena layout
+  struct Item { void** dst; size_t bytes; };
+  EngState& h = e->h_st;
+  std::memset(&h, 0, sizeof(h));
+  long long fbytes_total = 0;
+  std::vector<Item> items;
+  const int ms = e->max_slots;
+  const int mv = 2 * ms + 2;
+  items.push_back({(void**)&h.slot_model, size_t(ms) * 4});
+  items.push_back({(void**)&h.slot_off, size_t(ms) * 4});
+  items.push_back({(void**)&h.mv_kind, size_t(mv) * 4});
+  items.push_back({(void**)&h.mv_model, size_t(mv) * 4});
+  items.push_back({(void**)&h.mv_src, size_t(mv) * 4});
+  items.push_back({(void**)&h.mv_dst, size_t(mv) * 4});
+  items.push_back({(void**)&h.mv_len, size_t(mv) * 4});
+  items.push_back({(void**)&h.mv_pre, size_t(mv) * 4});
+  const size_t nmod = std::max(1, n_models);
+  items.push_back({(void**)&h.rank, nmod * 4});
+  items.push_back({(void**)&h.pool_off, nmod * N * 8});
+  items.push_back({(void**)&h.gram_off, nmod * 8});
+  items.push_back({(void**)&h.status, nmod * 4});
+  items.push_back({(void**)&h.iters, nmod * 4});
+  items.push_back({(void**)&h.failed, nmod * 4});
+  items.push_back({(void**)&h.fresh, nmod * 4});
+  items.push_back({(void**)&h.retire_seq, nmod * 4});
+  items.push_back({(void**)&h.f_prev, nmod * 8});
+  items.push_back({(void**)&h.err, nmod * 8});
+  items.push_back({(void**)&h.fit, nmod * 8});
+  items.push_back({(void**)&h.t_admit, nmod * 8});
+  items.push_back({(void**)&h.t_retire, nmod * 8});
+  items.push_back({(void**)&h.grams, size_t(N) * e->gram_stride * 8});
+  items.push_back({(void**)&h.pool, size_t(std::max<long long>(po, 1)) * 8});
+  for (int n = 0; n < N; ++n) {
+    items.push_back({(void**)&h.F[n], size_t(t->dims[n]) * e->ld * 8});
+    fbytes_total += t->dims[n] * e->ld * 8;
+  }
+  items.push_back({(void**)&h.Mout, size_t(maxI) * e->ld * 8});
+  items.push_back({(void**)&h.scratch,
+                   size_t(e->upd_grid) * (2 * rmax * rmax + rmax) * 8});
+  items.push_back({(void**)&h.tr_width, size_t(e->trace_cap) * 4});
+  items.push_back({(void**)&h.tr_active, size_t(e->trace_cap) * 4});
+  items.push_back({(void**)&h.tr_time, size_t(e->trace_cap) * 8});
+  items.push_back({(void**)&e->d_lam, size_t(e->lam_elems) * 8});
+  items.push_back({(void**)&e->d_lam_off, nmod * 8});
+  size_t total = 0;
+  for (auto& it : items) total = align_up(total, 256) + it.bytes;
+  CALS_CUDA_TRY(cudaMalloc(&e->d_block, total));
+  CALS_CUDA_TRY(cudaMemset(e->d_block, 0, total));
+  size_t off = 0;
+  for (auto& it : items) {
+    off = align_up(off, 256);
+    *it.dst = static_cast<char*>(e->d_block) + off;
+    off += it.bytes;
+  }
+  CALS_CUDA_TRY(cudaMalloc(&e->d_st, sizeof(EngState)));
+  CALS_CUDA_TRY(cudaHostAlloc(&e->h_done, 64, cudaHostAllocMapped));
+  CALS_CUDA_TRY(cudaHostGetDevicePointer(&e->d_done_alias, e->h_done, 0));
+
+  // constant tables
+  if (n_models > 0) {
+    CALS_CUDA_TRY(cudaMemcpy((void*)h.rank, ranks, size_t(n_models) * 4, cudaMemcpyHostToDevice));
+    CALS_CUDA_TRY(cudaMemcpy((void*)h.pool_off, e->pool_off.data(), size_t(n_models) * N * 8,
+                             cudaMemcpyHostToDevice));
+    CALS_CUDA_TRY(cudaMemcpy((void*)h.gram_off, e->gram_off.data(), size_t(n_models) * 8,
+                             cudaMemcpyHostToDevice));
+    CALS_CUDA_TRY(cudaMemcpy(e->d_lam_off, e->lam_off.data(), size_t(n_models) * 8,
+                             cudaMemcpyHostToDevice));
+  }
+  h.order = N;
+  h.n_models = n_models;
+  h.capacity = capacity;
+  h.max_slots = ms;
+  h.max_rank = rmax;
+  h.ld = e->ld;
+  for (int n = 0; n < N; ++n) h.dims[n] = t->dims[n];
+  h.gram_stride = e->gram_stride;
+  h.tr_cap = e->trace_cap;
+  h.host_done = e->d_done_alias;
+
+  // MTTKRP workspace + variants (chosen for the capacity width)
+  e->ws_bytes = 256;
+  for (int n = 0; n < N; ++n) {
+    e->ws_bytes = std::max(e->ws_bytes, mttkrp_workspace_bytes(*t, n, e->ld));
+    e->variants[n] = choose_variant(t->plans[n].M, capacity, t->plans[n].S);
+  }
+  CALS_CUDA_TRY(cudaMalloc(&e->d_ws, e->ws_bytes));
+  *out = e.release();
+  return kOk;
+}
+
+static int engine_reset(Engine* e, double tol, int max_iterations, double sqnorm,
+                        cudaStream_t stream) {
+  EngState& h = e->h_st;
+  h.width = h.n_active = h.queue_head = h.n_retired = h.plans_done = h.done = 0;
+  h.old_width = h.n_moves = h.move_elems = 0;
+  h.tol = tol;
+  h.max_iterations = max_iterations;
+  h.sqnorm = sqnorm;
+  const size_t nm = std::max(1, e->n_models);
+  CALS_CUDA_TRY(cudaMemsetAsync(h.status, 0, nm * 4, stream));
+  CALS_CUDA_TRY(cudaMemsetAsync(h.iters, 0, nm * 4, stream));
+  CALS_CUDA_TRY(cudaMemsetAsync(h.failed, 0, nm * 4, stream));
+  CALS_CUDA_TRY(cudaMemsetAsync(h.fresh, 0, nm * 4, stream));
+  CALS_CUDA_TRY(cudaMemsetAsync(h.retire_seq, 0xff, nm * 4, stream));
+  std::vector<double> minf(nm, -INFINITY), pinf(nm, INFINITY);
+  // f_prev = -inf, err = +inf, fit = -inf (driver.py:56-67)
+  CALS_CUDA_TRY(cudaMemcpyAsync(h.f_prev, minf.data(), nm * 8, cudaMemcpyHostToDevice, stream));
+  CALS_CUDA_TRY(cudaMemcpyAsync(h.err, pinf.data(), nm * 8, cudaMemcpyHostToDevice, stream));
+  CALS_CUDA_TRY(cudaMemcpyAsync(h.fit, minf.data(), nm * 8, cudaMemcpyHostToDevice, stream));
+  CALS_CUDA_TRY(cudaMemcpyAsync(e->d_st, &h, sizeof(EngState), cudaMemcpyHostToDevice, stream));
+  CALS_CUDA_TRY(cudaStreamSynchronize(stream));  // the host vectors above are stack-owned
+  *e->h_done = 0;
+  return kOk;
+}
+
+static int enqueue_iteration(Engine* e, cudaStream_t stream) {
+  Tensor& t = *e->t;
+  const int N = e->order;
+  FactorSet fs{};
+  for (int n = 0; n < N; ++n) fs.ptr[n] = e->h_st.F[n];
+  fs.ld = e->ld;
+  const int* wptr = &e->d_st->width;
+  for (int n = 0; n < N; ++n) {
+    int rc = launch_mttkrp(t, n, fs, 0, wptr, e->capacity, e->h_st.Mout, e->ld, e->d_ws,
+                           e->ws_bytes, e->variants[n], stream);
+    if (rc) return rc;
+    engine_update_kernel<<<e->upd_grid, kUpdThreads, e->upd_smem, stream>>>(e->d_st, n,
+                                                                            e->upd_nthr);
+    CALS_CUDA_TRY(cudaGetLastError());
+  }
+  engine_plan_kernel<<<1, 32, 0, stream>>>(e->d_st);
+  CALS_CUDA_TRY(cudaGetLastError());
+  engine_move_kernel<<<e->move_grid, 256, e->move_smem, stream>>>(e->d_st);
+  CALS_CUDA_TRY(cudaGetLastError());
+  return kOk;
+}
+
+static int engine_capture(Engine* e, cudaStream_t stream) {
+  if (e->exec) return kOk;
+  // capture on a private stream (the caller's stream may be the legacy default stream)
+  cudaStream_t cs;
+  CALS_CUDA_TRY(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
+  CALS_CUDA_TRY(cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal));
+  int rc = enqueue_iteration(e, cs);
+  cudaGraph_t g = nullptr;
+  cudaError_t ce = cudaStreamEndCapture(cs, &g);
+  cudaStreamDestroy(cs);
+  if (rc) {
+    if (g) cudaGraphDestroy(g);
+    return rc;
+  }
+  CALS_CUDA_TRY(ce);
+  e->graph = g;
+  CALS_CUDA_TRY(cudaGraphInstantiate(&e->exec, g, 0));
+  (void)stream;
+  return kOk;
+}
+
+// Run every queued model to retirement.  `pool` must already hold the
+// starting factors (per model, per mode, row-major I_n x R_k).
+static int engine_run(Engine* e, double tol, int max_iterations, double sqnorm, int use_graph,
+                      cudaStream_t stream, int* iterations_out) {
+  CALS_CHECK(max_iterations >= 1, kErrInvalid, "max_iterations must be >= 1");
+  CALS_CHECK(sqnorm > 0.0, kErrInvalid, "tensor squared norm must be positive");
+  int rc = engine_reset(e, tol, max_iterations, sqnorm, stream);
+  if (rc) return rc;
+  if (e->n_models == 0) {
+    if (iterations_out) *iterations_out = 0;
+    return kOk;
+  }
+  // initial admission
+  engine_plan_kernel<<<1, 32, 0, stream>>>(e->d_st);
+  engine_move_kernel<<<e->move_grid, 256, e->move_smem, stream>>>(e->d_st);
+  CALS_CUDA_TRY(cudaGetLastError());
+  if (use_graph) {
+    rc = engine_capture(e, stream);
+    if (rc) return rc;
+  }
+  const int kLook = 3;
+  cudaEvent_t ev[kLook];
+  for (int i = 0; i < kLook; ++i)
+    CALS_CUDA_TRY(cudaEventCreateWithFlags(&ev[i], cudaEventDisableTiming));
+  long long launched = 0;
+  // Upper bound on driver iterations: every model needs <= max_iterations.
+  const long long bound = (long long)max_iterations * std::max(1, e->n_models) + 2;
+  int result = kOk;
+  while (launched < bound) {
+    if (use_graph) {
+      cudaError_t ce = cudaGraphLaunch(e->exec, stream);
+      if (ce != cudaSuccess) {
+        set_error(std::string("cudaGraphLaunch: ") + cudaGetErrorString(ce));
+        result = kErrCuda;
+        break;
+      }
+    } else {
+      rc = enqueue_iteration(e, stream);
+      if (rc) { result = rc; break; }
+    }
+    cudaEventRecord(ev[launched % kLook], stream);
+    ++launched;
+    if (launched >= kLook) {
+      cudaError_t ce = cudaEventSynchronize(ev[(launched - kLook) % kLook]);
+      if (ce != cudaSuccess) {
+        set_error(std::string("engine iteration failed: ") + cudaGetErrorString(ce));
+        result = kErrCuda;
+        break;
+      }
+      if (*(volatile int*)e->h_done) break;
+    }
+  }
+  cudaError_t ce = cudaStreamSynchronize(stream);
+  for (int i = 0; i < kLook; ++i) cudaEventDestroy(ev[i]);
+  if (result) return result;
+  CALS_CUDA_TRY(ce);
+  CALS_CHECK(*(volatile int*)e->h_done, kErrInvalid, "engine did not terminate");
+  int plans = 0;
+  CALS_CUDA_TRY(cudaMemcpy(&plans, &e->d_st->plans_done, 4, cudaMemcpyDeviceToHost));
+  e->last_iterations = plans - 1;
+  if (iterations_out) *iterations_out = plans - 1;
+  return kOk;
+}
+
+}  // namespace cals
+
+// ============================================================ C ABI ========
+#include "../../include/cals_b200.h"
+
+using namespace cals;
+
+struct cals_tensor { Tensor* t; };
+struct cals_engine { Engine* e; };
+
+extern "C" {
+
+int cals_abi_version(void) { return CALS_B200_ABI_VERSION; }
+
+const char* cals_last_error(void) { return get_error(); }
+
+int cals_tensor_create(int order, const int64_t* dims, const double* host_data,
+                       const double* device_data, void* stream, cals_tensor** out) {
+  Tensor* t = nullptr;
+  int rc = tensor_create(order, dims, host_data, device_data, (cudaStream_t)stream, &t);
+  if (rc) return rc;
+  *out = new cals_tensor{t};
+  return kOk;
+}
+
+int cals_tensor_destroy(cals_tensor* t) {
+  if (t) {
+    tensor_destroy(t->t);
+    delete t;
+  }
+  return kOk;
+}
+
+int cals_tensor_sqnorm(cals_tensor* t, void* stream, double* out) {
+  CALS_CHECK(t && out, kErrInvalid, "null argument");
+  return tensor_sqnorm(t->t, (cudaStream_t)stream, out);
+}
+
+int cals_tensor_data(cals_tensor* t, double** data, int64_t* padded_i0) {
+  CALS_CHECK(t, kErrInvalid, "null tensor");
+  if (data) *data = t->t->data;
+  if (padded_i0) *padded_i0 = t->t->i0p;
+  return kOk;
+}
+
+int cals_mttkrp_workspace_bytes(cals_tensor* t, int mode, int64_t capacity, size_t* bytes) {
+  CALS_CHECK(t && bytes, kErrInvalid, "null argument");
+  CALS_CHECK(mode >= 0 && mode < t->t->order, kErrInvalid, "mode out of range");
+  *bytes = mttkrp_workspace_bytes(*t->t, mode, (capacity + 1) / 2 * 2);
+  return kOk;
+}
+
+int cals_mttkrp(cals_tensor* t, int mode, int width, const double* const* factors, int64_t ldf,
+                double* out, int64_t ldo, double* workspace, size_t workspace_bytes,
+                int variant, void* stream) {
+  CALS_CHECK(t && factors && out, kErrInvalid, "null argument");
+  CALS_CHECK(mode >= 0 && mode < t->t->order, kErrInvalid, "mode out of range");
+  CALS_CHECK(width >= 1 && width <= ldf, kErrInvalid, "width must be in [1, ldf]");
+  CALS_CHECK(variant < num_variants(), kErrInvalid, "unknown variant");
+  FactorSet fs{};
+  for (int n = 0; n < t->t->order; ++n) fs.ptr[n] = factors[n];
+  fs.ld = ldf;
+  return launch_mttkrp(*t->t, mode, fs, width, nullptr, ldf, out, ldo, workspace,
+                       workspace_bytes, variant, (cudaStream_t)stream);
+}
+
+int cals_mttkrp_variants(int* count) {
+  CALS_CHECK(count, kErrInvalid, "null argument");
+  *count = num_variants();
+  return kOk;
+}
+
+int cals_update_factor(int rows, int rank, const double* m, int64_t ldm, const double* h,
+                       double* a, int64_t lda, double* scratch, int* status, void* stream) {
+  CALS_CHECK(rows >= 0 && rank >= 1 && rank <= 128, kErrInvalid, "rank must be in [1, 128]");
+  CALS_CHECK(m && h && a && scratch && status, kErrInvalid, "null argument");
+  const int nthr = pick_nthr(rank);
+  const size_t smem = size_t(rank) * rank * 8 + size_t(rank) * nthr * 8;
+  CALS_CUDA_TRY(cudaFuncSetAttribute(standalone_update_kernel,
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  standalone_update_kernel<<<1, kUpdThreads, smem, (cudaStream_t)stream>>>(
+      m, ldm, rows, rank, h, a, lda, scratch, nthr, status);
+  CALS_CUDA_TRY(cudaGetLastError());
+  return kOk;
+}
+
+size_t cals_update_scratch_bytes(int rank) { return size_t(3 * rank * rank + rank) * 8; }
+
+int cals_engine_create(cals_tensor* t, int r_star, int n_models, const int32_t* ranks,
+                       int trace_capacity, cals_engine** out) {
+  CALS_CHECK(t && out, kErrInvalid, "null argument");
+  Engine* e = nullptr;
+  int rc = engine_create(t->t, r_star, n_models, ranks, trace_capacity, &e);
+  if (rc) return rc;
+  *out = new cals_engine{e};
+  return kOk;
+}
+
+int cals_engine_destroy(cals_engine* e) {
+  if (e) {
+    engine_free(e->e);
+    delete e;
+  }
+  return kOk;
+}
+
+int cals_engine_pool(cals_engine* e, double** pool, int64_t* elems) {
+  CALS_CHECK(e, kErrInvalid, "null engine");
+  if (pool) *pool = e->e->h_st.pool;
+  if (elems) *elems = e->e->pool_elems;
+  return kOk;
+}
+
+int cals_engine_load_pool(cals_engine* e, const double* src, int src_is_device, void* stream) {
+  CALS_CHECK(e && src, kErrInvalid, "null argument");
+  CALS_CUDA_TRY(cudaMemcpyAsync(e->e->h_st.pool, src, size_t(e->e->pool_elems) * 8,
+                                src_is_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice,
+                                (cudaStream_t)stream));
+  return kOk;
+}
+
+int cals_engine_run(cals_engine* e, double tol, int max_iterations, double sqnorm, int use_graph,
+                    void* stream, int* iterations) {
+  CALS_CHECK(e, kErrInvalid, "null engine");
+  return engine_run(e->e, tol, max_iterations, sqnorm, use_graph, (cudaStream_t)stream,
+                    iterations);
+}
+
+int cals_engine_results(cals_engine* e, double* pool, int32_t* status, int32_t* iterations,
+                        double* error, double* fit, int32_t* retire_seq, double* seconds_active,
+                        double* lambdas, void* stream) {
+  CALS_CHECK(e, kErrInvalid, "null engine");
+  Engine* g = e->e;
+  cudaStream_t s = (cudaStream_t)stream;
+  const size_t nm = size_t(g->n_models);
+  if (nm == 0) return kOk;
+  const EngState& h = g->h_st;
+  if (lambdas) {
+    lambdas_kernel<<<std::min<int>(g->n_models, 1024), 32, 0, s>>>(g->d_st, g->d_lam_off,
+                                                                 g->d_lam);
+    CALS_CUDA_TRY(cudaGetLastError());
+    CALS_CUDA_TRY(cudaMemcpyAsync(lambdas, g->d_lam, size_t(g->lam_elems) * 8,
+                                  cudaMemcpyDeviceToHost, s));
+  }
+  if (pool)
+    CALS_CUDA_TRY(cudaMemcpyAsync(pool, h.pool, size_t(g->pool_elems) * 8, cudaMemcpyDeviceToHost, s));
+  if (status) CALS_CUDA_TRY(cudaMemcpyAsync(status, h.status, nm * 4, cudaMemcpyDeviceToHost, s));
+  if (iterations)
+    CALS_CUDA_TRY(cudaMemcpyAsync(iterations, h.iters, nm * 4, cudaMemcpyDeviceToHost, s));
+  if (error) CALS_CUDA_TRY(cudaMemcpyAsync(error, h.err, nm * 8, cudaMemcpyDeviceToHost, s));
+  if (fit) CALS_CUDA_TRY(cudaMemcpyAsync(fit, h.fit, nm * 8, cudaMemcpyDeviceToHost, s));
+  if (retire_seq)
+    CALS_CUDA_TRY(cudaMemcpyAsync(retire_seq, h.retire_seq, nm * 4, cudaMemcpyDeviceToHost, s));
+  std::vector<unsigned long long> ta(nm), tr(nm);
+  if (seconds_active) {
+    CALS_CUDA_TRY(cudaMemcpyAsync(ta.data(), h.t_admit, nm * 8, cudaMemcpyDeviceToHost, s));
+    CALS_CUDA_TRY(cudaMemcpyAsync(tr.data(), h.t_retire, nm * 8, cudaMemcpyDeviceToHost, s));
+  }
+  CALS_CUDA_TRY(cudaStreamSynchronize(s));
+  if (seconds_active)
+    for (size_t k = 0; k < nm; ++k) seconds_active[k] = (double)(tr[k] - ta[k]) * 1e-9;
+  return kOk;
+}
+
+int cals_engine_trace(cals_engine* e, int32_t* widths, int32_t* n_active, double* seconds,
+                      int capacity, int* count) {
+  CALS_CHECK(e && count, kErrInvalid, "null argument");
+  Engine* g = e->e;
+  int plans = 0;
+  CALS_CUDA_TRY(cudaMemcpy(&plans, &g->d_st->plans_done, 4, cudaMemcpyDeviceToHost));
+  const int recs = std::min(plans, g->trace_cap);
+  const int iters = std::max(0, recs - 1);
+  *count = iters;
+  if (iters == 0 || capacity <= 0) return kOk;
+  std::vector<int> w(recs), a(recs);
+  std::vector<unsigned long long> tt(recs);
+  CALS_CUDA_TRY(cudaMemcpy(w.data(), g->h_st.tr_width, recs * 4, cudaMemcpyDeviceToHost));
+  CALS_CUDA_TRY(cudaMemcpy(a.data(), g->h_st.tr_active, recs * 4, cudaMemcpyDeviceToHost));
+  CALS_CUDA_TRY(cudaMemcpy(tt.data(), g->h_st.tr_time, recs * 8, cudaMemcpyDeviceToHost));
+  for (int i = 0; i < std::min(iters, capacity); ++i) {
+    if (widths) widths[i] = w[i];
+    if (n_active) n_active[i] = a[i];
+    if (seconds) seconds[i] = (double)(tt[i + 1] - tt[i]) * 1e-9;
+  }
+  return kOk;
+}
+
+int cals_engine_variant(cals_engine* e, int mode, int* variant, int* bm, int* bn, int* splits) {
+  CALS_CHECK(e && mode >= 0 && mode < e->e->order, kErrInvalid, "bad argument");
+  const int v = e->e->variants[mode];
+  if (variant) *variant = v;
+  if (bm) *bm = variant_info(v).BM;
+  if (bn) *bn = variant_info(v).BN;
+  if (splits) *splits = e->e->t->plans[mode].S;
+  return kOk;
+}
+
+}  // extern "C"

@@ -1,0 +1,91 @@
+// Host-side internal interfaces shared by the CALS translation units.
+#pragma once
+
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <map>
+#include <mutex>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "common.cuh"
+
+namespace cals {
+
+constexpr int kMaxOrder = 8;
+
+// One mode's MTTKRP expressed on the contiguous 3-D view of the tensor
+// (see mttkrp.cuh).  lo_modes / hi_modes list the factor modes whose
+// Khatri-Rao product forms Lo / Hi, lowest mode first (= fastest row index).
+struct ModePlan {
+  int mode = 0;
+  int role = 0;
+  long long D[3] = {1, 1, 1};
+  long long M = 0, Dp = 0, Dq = 0;
+  int S = 1;
+  std::vector<int> lo_modes, hi_modes;
+  bool lo_direct() const { return lo_modes.size() == 1; }
+  bool hi_direct() const { return hi_modes.size() == 1; }
+  bool hi_ones() const { return hi_modes.empty(); }
+};
+
+// Device-resident dense tensor, mode-0 fastest, I0 padded to even so every
+// 3-D view has 16-byte aligned TMA strides.  Zero padding contributes nothing.
+struct Tensor {
+  int device = 0;
+  int order = 0;
+  long long dims[kMaxOrder] = {0};
+  long long i0p = 0;       // padded leading extent
+  long long numel = 0;     // logical element count
+  double* data = nullptr;  // [i0p * prod(dims[1:])]
+  bool owned = false;
+  double sqnorm = -1.0;
+  std::vector<ModePlan> plans;
+  // A-operand tensor maps cached per (mode, variant)
+  std::map<std::pair<int, int>, CUtensorMap> amaps;
+  std::mutex mu;
+};
+
+int tensor_create(int order, const int64_t* dims, const double* host, const double* dev,
+                  cudaStream_t stream, Tensor** out);
+void tensor_destroy(Tensor* t);
+int tensor_sqnorm(Tensor* t, cudaStream_t stream, double* out);
+ModePlan make_plan(const Tensor& t, int mode);
+
+// MTTKRP variants ------------------------------------------------------------
+struct VariantInfo {
+  int MI, NI, WM, WN;
+  int BM, BN;
+};
+int num_variants();
+const VariantInfo& variant_info(int v);
+int choose_variant(long long M, long long width_hint, int S);
+
+// Workspace bytes the MTTKRP of `mode` needs at width `cap` (partials + KRPs).
+size_t mttkrp_workspace_bytes(const Tensor& t, int mode, long long cap);
+
+struct FactorSet {
+  const double* ptr[kMaxOrder];  // row-major [I_n][ld] factor buffers
+  long long ld;                  // leading dimension (columns), even
+};
+
+// Launch one fused MTTKRP (+ split reduction) on `stream`.  `width` is used
+// when width_ptr is null; otherwise the kernels read the active width from
+// device memory (engine path, graph-capturable).  `cap` bounds the width and
+// sizes the grid.
+int launch_mttkrp(Tensor& t, int mode, const FactorSet& f, int width, const int* width_ptr,
+                  long long cap, double* out, long long ldo, double* workspace,
+                  size_t workspace_bytes, int variant, cudaStream_t stream);
+
+// Tensor maps ------------------------------------------------------------------
+int encode_map_2d(CUtensorMap* m, const double* base, long long inner, long long outer,
+                  long long ld_elems, int box_inner, int box_outer);
+int encode_map_3d(CUtensorMap* m, const double* base, long long d0, long long d1, long long d2,
+                  int b0, int b1, int b2);
+
+int sm_count(int device);
+
+}  // namespace cals

@@ -1,0 +1,514 @@
+// Host side of the fused MTTKRP: tensor upload/padding, per-mode plans, TMA
+// descriptor encoding, variant choice and launch (kernels in mttkrp.cuh).
+#include <cudaTypedefs.h>
+
+#include <algorithm>
+#include <cstring>
+#include <mutex>
+
+#include "internal.h"
+#include "mttkrp.cuh"
+
+namespace cals {
+
+// ---------------------------------------------------------------- errors --
+static thread_local std::string g_err;
+void set_error(const std::string& msg) { g_err = msg; }
+const char* get_error() { return g_err.c_str(); }
+
+int sm_count(int device) {
+  static int cached[64] = {0};
+  if (device < 0 || device >= 64) return 148;
+  if (!cached[device]) {
+    int v = 0;
+    if (cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, device) != cudaSuccess || v <= 0)
+      v = 148;
+    cached[device] = v;
+  }
+  return cached[device];
+}
+
+// ------------------------------------------------------------ tensor maps --
+static PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    cudaDriverEntryPointQueryResult q;
+    void* p = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) ==
+            cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  });
+  return fn;
+}
+
+int encode_map_2d(CUtensorMap* m, const double* base, long long inner, long long outer,
+                  long long ld_elems, int box_inner, int box_outer) {
+  auto enc = get_encode();
+  CALS_CHECK(enc, kErrCuda, "cuTensorMapEncodeTiled unavailable");
+  cuuint64_t dims[2] = {(cuuint64_t)inner, (cuuint64_t)outer};
+  cuuint64_t strides[1] = {(cuuint64_t)ld_elems * 8};
+  cuuint32_t box[2] = {(cuuint32_t)box_inner, (cuuint32_t)box_outer};
+  cuuint32_t es[2] = {1, 1};
+  CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<double*>(base), dims, strides,
+                   box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  CALS_CHECK(r == CUDA_SUCCESS, kErrCuda,
+             "cuTensorMapEncodeTiled(2d) failed: code " + std::to_string((int)r) + " inner=" +
+                 std::to_string(inner) + " outer=" + std::to_string(outer) +
+                 " ld=" + std::to_string(ld_elems));
+  return kOk;
+}
+
+int encode_map_3d(CUtensorMap* m, const double* base, long long d0, long long d1, long long d2,
+                  int b0, int b1, int b2) {
+  auto enc = get_encode();
+  CALS_CHECK(enc, kErrCuda, "cuTensorMapEncodeTiled unavailable");
+  cuuint64_t dims[3] = {(cuuint64_t)d0, (cuuint64_t)d1, (cuuint64_t)d2};
+  cuuint64_t strides[2] = {(cuuint64_t)d0 * 8, (cuuint64_t)(d0 * d1) * 8};
+  cuuint32_t box[3] = {(cuuint32_t)b0, (cuuint32_t)b1, (cuuint32_t)b2};
+  cuuint32_t es[3] = {1, 1, 1};
+  CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, const_cast<double*>(base), dims, strides,
+                   box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  CALS_CHECK(r == CUDA_SUCCESS, kErrCuda,
+             "cuTensorMapEncodeTiled(3d) failed: code " + std::to_string((int)r));
+  return kOk;
+}
+
+// ------------------------------------------------------------------ tensor --
+__global__ void sqnorm_partial_kernel(const double* __restrict__ x, long long n,
+                                      double* __restrict__ part) {
+  double s = 0.0;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x)
+    s = fma(x[i], x[i], s);
+  __shared__ double red[256];
+  red[threadIdx.x] = s;
+  __syncthreads();
+  for (int w = blockDim.x / 2; w > 0; w >>= 1) {
+    if (threadIdx.x < w) red[threadIdx.x] += red[threadIdx.x + w];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) part[blockIdx.x] = red[0];
+}
+
+__global__ void sum_kernel(const double* __restrict__ part, int n, double* out) {
+  if (threadIdx.x == 0 && blockIdx.x == 0) {
+    double s = 0.0;
+    for (int i = 0; i < n; ++i) s += part[i];
+    *out = s;
+  }
+}
+
+ModePlan make_plan(const Tensor& t, int mode) {
+  ModePlan p;
+  const int N = t.order;
+  p.mode = mode;
+  auto prod = [&](int a, int b) {  // prod dims[a..b)
+    long long v = 1;
+    for (int i = a; i < b; ++i) v *= t.dims[i];
+    return v;
+  };
+  if (mode == 0) {
+    p.role = kRoleFirst;
+    p.D[0] = t.i0p;
+    p.D[1] = t.dims[1];
+    p.D[2] = prod(2, N);
+    p.M = t.dims[0];
+    p.Dp = p.D[1];
+    p.Dq = p.D[2];
+    p.lo_modes = {1};
+    for (int i = 2; i < N; ++i) p.hi_modes.push_back(i);
+  } else if (mode == N - 1) {
+    p.role = kRoleLast;
+    p.D[0] = t.i0p;
+    p.D[1] = prod(1, N - 1);
+    p.D[2] = t.dims[N - 1];
+    p.M = t.dims[N - 1];
+    p.Dp = p.D[0];
+    p.Dq = p.D[1];
+    p.lo_modes = {0};
+    for (int i = 1; i < N - 1; ++i) p.hi_modes.push_back(i);
+  } else {
+    p.role = kRoleMiddle;
+    p.D[0] = t.i0p * prod(1, mode);
+    p.D[1] = t.dims[mode];
+    p.D[2] = prod(mode + 1, N);
+    p.M = t.dims[mode];
+    p.Dp = p.D[0];
+    p.Dq = p.D[2];
+    for (int i = 0; i < mode; ++i) p.lo_modes.push_back(i);
+    for (int i = mode + 1; i < N; ++i) p.hi_modes.push_back(i);
+  }
+  // q splits: a function of the shape only (never of the active width) so the
+  // fused result of a column block is bitwise independent of its neighbours.
+  p.S = (int)std::min<long long>(p.Dq, 32);
+  if (p.S < 1) p.S = 1;
+  return p;
+}
+
+__global__ void pad_copy_kernel(const double* __restrict__ src, long long i0, long long i0p,
+                                long long rows, double* __restrict__ dst) {
+  const long long n = i0p * rows;
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < n;
+       e += (long long)gridDim.x * blockDim.x) {
+    const long long i = e % i0p, row = e / i0p;
+    dst[e] = i < i0 ? src[row * i0 + i] : 0.0;
+  }
+}
+
+int tensor_create(int order, const int64_t* dims, const double* host, const double* dev,
+                  cudaStream_t stream, Tensor** out) {
+  CALS_CHECK(out != nullptr, kErrInvalid, "null output handle");
+  CALS_CHECK(order >= 2 && order <= kMaxOrder, kErrInvalid,
+             "tensor order must be in [2, 8], got " + std::to_string(order));
+  CALS_CHECK((host != nullptr) != (dev != nullptr), kErrInvalid,
+             "exactly one of host / device data must be given");
+  std::unique_ptr<Tensor> t(new Tensor());
+  CALS_CUDA_TRY(cudaGetDevice(&t->device));
+  t->order = order;
+  long long rest = 1;
+  for (int i = 0; i < order; ++i) {
+    CALS_CHECK(dims[i] >= 1, kErrInvalid, "all extents must be >= 1");
+    t->dims[i] = dims[i];
+    if (i > 0) rest *= dims[i];
+  }
+  t->numel = dims[0] * rest;
+  t->i0p = dims[0] + (dims[0] & 1);
+  const bool aligned_dev =
+      dev && t->i0p == dims[0] && (reinterpret_cast<uintptr_t>(dev) % 16 == 0);
+  if (aligned_dev) {
+    t->data = const_cast<double*>(dev);  // borrowed
+  } else {
+    const size_t bytes = size_t(t->i0p) * size_t(rest) * 8;
+    CALS_CUDA_TRY(cudaMalloc(&t->data, bytes));
+    t->owned = true;
+    if (host) {
+      CALS_CUDA_TRY(cudaMemcpy2DAsync(t->data, t->i0p * 8, host, dims[0] * 8, dims[0] * 8,
+                                      rest, cudaMemcpyHostToDevice, stream));
+      if (t->i0p != dims[0]) {
+        // zero the pad column (one double per row)
+        CALS_CUDA_TRY(cudaMemset2DAsync(t->data + dims[0], t->i0p * 8, 0, 8, rest, stream));
+      }
+    } else {
+      const int sms = sm_count(t->device);
+      pad_copy_kernel<<<sms * 4, 256, 0, stream>>>(dev, dims[0], t->i0p, rest, t->data);
+      CALS_CUDA_TRY(cudaGetLastError());
+    }
+  }
+  for (int n = 0; n < order; ++n) t->plans.push_back(make_plan(*t, n));
+  *out = t.release();
+  return kOk;
+}
+
+void tensor_destroy(Tensor* t) {
+  if (!t) return;
+  if (t->owned && t->data) cudaFree(t->data);
+  delete t;
+}
+
+int tensor_sqnorm(Tensor* t, cudaStream_t stream, double* out) {
+  if (t->sqnorm < 0) {
+    const long long n = t->i0p * (t->numel / t->dims[0]);  // padding is zero
+    const int blocks = 1024;
+    double* buf = nullptr;
+    CALS_CUDA_TRY(cudaMallocAsync(&buf, (blocks + 1) * sizeof(double), stream));
+    sqnorm_partial_kernel<<<blocks, 256, 0, stream>>>(t->data, n, buf);
+    sum_kernel<<<1, 32, 0, stream>>>(buf, blocks, buf + blocks);
+    double h = 0;
+    CALS_CUDA_TRY(cudaMemcpyAsync(&h, buf + blocks, 8, cudaMemcpyDeviceToHost, stream));
+    CALS_CUDA_TRY(cudaStreamSynchronize(stream));
+    CALS_CUDA_TRY(cudaFreeAsync(buf, stream));
+    t->sqnorm = h;
+  }
+  *out = t->sqnorm;
+  return kOk;
+}
+
+// ---------------------------------------------------------------- variants --
+using LaunchFn = cudaError_t (*)(dim3, const CUtensorMap&, const CUtensorMap&, const MttkrpArgs&,
+                                 bool kc, cudaStream_t);
+
+template <int MI, int NI, int WM, int WN>
+static cudaError_t launch_variant(dim3 grid, const CUtensorMap& a, const CUtensorMap& b,
+                                  const MttkrpArgs& args, bool kc, cudaStream_t stream) {
+  using C = TileCfg<MI, NI, WM, WN>;
+  const size_t smem = C::kSmemBytes;
+  static std::once_flag once;
+  static cudaError_t cfg = cudaSuccess;
+  std::call_once(once, [&] {
+    cfg = cudaFuncSetAttribute(mttkrp_dmma_kernel<MI, NI, WM, WN, true>,
+                               cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (cfg == cudaSuccess)
+      cfg = cudaFuncSetAttribute(mttkrp_dmma_kernel<MI, NI, WM, WN, false>,
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  });
+  if (cfg != cudaSuccess) return cfg;
+  if (kc)
+    mttkrp_dmma_kernel<MI, NI, WM, WN, true><<<grid, C::kThreads, smem, stream>>>(a, b, args);
+  else
+    mttkrp_dmma_kernel<MI, NI, WM, WN, false><<<grid, C::kThreads, smem, stream>>>(a, b, args);
+  return cudaGetLastError();
+}
+
+template <int MI, int NI, int WM, int WN>
+static int occupancy_variant() {
+  using C = TileCfg<MI, NI, WM, WN>;
+  static int occ = -1;
+  static std::mutex mu;
+  std::lock_guard<std::mutex> lk(mu);
+  if (occ < 0) {
+    cudaFuncSetAttribute(mttkrp_dmma_kernel<MI, NI, WM, WN, true>,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::kSmemBytes);
+    int v = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(
+            &v, mttkrp_dmma_kernel<MI, NI, WM, WN, true>, C::kThreads, C::kSmemBytes) !=
+            cudaSuccess ||
+        v < 1)
+      v = 1;
+    occ = v;
+  }
+  return occ;
+}
+
+struct VariantEntry {
+  VariantInfo info;
+  LaunchFn launch;
+  int (*occupancy)();
+};
+
+#define CALS_VARIANT(MI, NI, WM, WN)                                               \
+  VariantEntry {                                                                   \
+    VariantInfo{MI, NI, WM, WN, 8 * MI * WM, 8 * NI * WN}, &launch_variant<MI, NI, WM, WN>, \
+        &occupancy_variant<MI, NI, WM, WN>                                         \
+  }
+
+static const VariantEntry kVariants[] = {
+    CALS_VARIANT(4, 4, 2, 2),  // 64 x 64
+    CALS_VARIANT(5, 3, 1, 4),  // 40 x 96
+    CALS_VARIANT(3, 4, 1, 4),  // 24 x 128
+    CALS_VARIANT(2, 4, 1, 4),  // 16 x 128
+    CALS_VARIANT(1, 4, 1, 4),  // 8 x 128
+};
+
+int num_variants() { return int(sizeof(kVariants) / sizeof(kVariants[0])); }
+const VariantInfo& variant_info(int v) { return kVariants[v].info; }
+
+int choose_variant(long long M, long long width_hint, int S) {
+  const long long slots = 2LL * sm_count(0);
+  long long best_cost = -1;
+  int best = 0;
+  for (int v = 0; v < num_variants(); ++v) {
+    const auto& vi = kVariants[v].info;
+    const long long tm = (M + vi.BM - 1) / vi.BM;
+    const long long tn = (std::max<long long>(width_hint, 1) + vi.BN - 1) / vi.BN;
+    const long long units = tm * tn * S;
+    const long long waves = (units + slots - 1) / slots;
+    // padded work per slot, plus a per-unit fixed cost (pipeline fill, epilogue)
+    const long long cost = waves * ((long long)vi.BM * vi.BN + 1024);
+    if (best_cost < 0 || cost < best_cost) {
+      best_cost = cost;
+      best = v;
+    }
+  }
+  return best;
+}
+
+// --------------------------------------------------------- KRP / reduction --
+struct KrpParts {
+  const double* ptr[kMaxOrder];
+  long long ext[kMaxOrder];    // extent used to decode the row index
+  long long valid[kMaxOrder];  // rows >= valid are zero (padding of mode 0)
+  int n;
+};
+
+__global__ void krp_rows_kernel(KrpParts parts, long long ld_in, long long rows, const int* wptr,
+                                int width, double* __restrict__ out, long long ldo) {
+  const int W = wptr ? *wptr : width;
+  const long long n = rows * W;
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < n;
+       e += (long long)gridDim.x * blockDim.x) {
+    const long long row = e / W;
+    const int c = int(e % W);
+    long long rem = row;
+    double v = 1.0;
+    for (int k = 0; k < parts.n; ++k) {
+      const long long idx = rem % parts.ext[k];
+      rem /= parts.ext[k];
+      v = idx < parts.valid[k] ? v * parts.ptr[k][idx * ld_in + c] : 0.0;
+    }
+    out[row * ldo + c] = v;
+  }
+}
+
+__global__ void fill_kernel(double* p, long long n, double v) {
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < n;
+       e += (long long)gridDim.x * blockDim.x)
+    p[e] = v;
+}
+
+__global__ void split_reduce_kernel(const double* __restrict__ part, long long part_stride, int S,
+                                    int M, long long ldp, const int* width_ptr, int width,
+                                    double* __restrict__ out, long long ldo) {
+  const int W = width_ptr ? *width_ptr : width;
+  const int hw = (W + 1) >> 1;  // column pairs
+  const long long n = (long long)M * hw;
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < n;
+       e += (long long)gridDim.x * blockDim.x) {
+    const int m = int(e / hw);
+    const int c = int(e % hw) * 2;
+    const double* src = part + (long long)m * ldp + c;
+    if (c + 1 < W) {
+      double2 acc = *reinterpret_cast<const double2*>(src);
+      for (int s = 1; s < S; ++s) {
+        const double2 v = *reinterpret_cast<const double2*>(src + s * part_stride);
+        acc.x += v.x;
+        acc.y += v.y;
+      }
+      *reinterpret_cast<double2*>(out + (long long)m * ldo + c) = acc;
+    } else {
+      double acc = src[0];
+      for (int s = 1; s < S; ++s) acc += src[s * part_stride];
+      out[(long long)m * ldo + c] = acc;
+    }
+  }
+}
+
+static long long lo_rows(const Tensor& t, const ModePlan& p) {
+  return p.lo_direct() ? t.dims[p.lo_modes[0]] : p.Dp;
+}
+
+size_t mttkrp_workspace_bytes(const Tensor& t, int mode, long long cap) {
+  const ModePlan& p = t.plans[mode];
+  const long long ld = (cap + 7) / 8 * 8;
+  size_t b = 0;
+  if (p.S > 1) b += size_t(p.S) * size_t(p.M) * size_t(ld) * 8;
+  if (!p.lo_direct()) b += size_t(p.Dp) * size_t(ld) * 8;
+  if (!p.hi_direct()) b += size_t(std::max<long long>(p.Dq, 1)) * size_t(ld) * 8;
+  return b + 256;
+}
+
+int launch_mttkrp(Tensor& t, int mode, const FactorSet& f, int width, const int* width_ptr,
+                  long long cap, double* out, long long ldo, double* workspace,
+                  size_t workspace_bytes, int variant, cudaStream_t stream) {
+  CALS_CHECK(mode >= 0 && mode < t.order, kErrInvalid, "mode out of range");
+  const ModePlan& p = t.plans[mode];
+  CALS_CHECK(f.ld % 2 == 0 && f.ld >= cap, kErrInvalid, "factor leading dimension must be even");
+  CALS_CHECK(ldo % 2 == 0 && ldo >= cap, kErrInvalid, "output leading dimension must be even");
+  CALS_CHECK(cap >= 1 && (width_ptr || (width >= 1 && width <= cap)), kErrInvalid,
+             "width must be in [1, capacity]");
+  CALS_CHECK(mttkrp_workspace_bytes(t, mode, f.ld) <= workspace_bytes || p.S == 1, kErrInvalid,
+             "MTTKRP workspace too small");
+  if (variant < 0) variant = choose_variant(p.M, cap, p.S);
+  const VariantEntry& ve = kVariants[variant];
+  const int sms = sm_count(t.device);
+
+  // carve the workspace
+  char* wsp = reinterpret_cast<char*>(workspace);
+  double* part = nullptr;
+  if (p.S > 1) {
+    part = reinterpret_cast<double*>(wsp);
+    wsp += size_t(p.S) * size_t(p.M) * size_t(f.ld) * 8;
+  }
+  const double* lo = nullptr;
+  const double* hi = nullptr;
+  long long lo_ld = f.ld, hi_ld = f.ld;
+  const long long lrows = lo_rows(t, p);
+  if (p.lo_direct()) {
+    lo = f.ptr[p.lo_modes[0]];
+  } else {
+    double* buf = reinterpret_cast<double*>(wsp);
+    wsp += size_t(p.Dp) * size_t(f.ld) * 8;
+    KrpParts kp{};
+    kp.n = (int)p.lo_modes.size();
+    for (int k = 0; k < kp.n; ++k) {
+      const int m = p.lo_modes[k];
+      kp.ptr[k] = f.ptr[m];
+      kp.ext[k] = m == 0 ? t.i0p : t.dims[m];
+      kp.valid[k] = t.dims[m];
+    }
+    krp_rows_kernel<<<sms * 8, 256, 0, stream>>>(kp, f.ld, p.Dp, width_ptr, width, buf, f.ld);
+    CALS_CUDA_TRY(cudaGetLastError());
+    lo = buf;
+  }
+  if (p.hi_direct()) {
+    hi = f.ptr[p.hi_modes[0]];
+  } else {
+    double* buf = reinterpret_cast<double*>(wsp);
+    wsp += size_t(std::max<long long>(p.Dq, 1)) * size_t(f.ld) * 8;
+    if (p.hi_ones()) {
+      fill_kernel<<<std::max<long long>(1, std::min<long long>(sms, (f.ld + 255) / 256)), 256, 0,
+                    stream>>>(buf, f.ld, 1.0);
+    } else {
+      KrpParts kp{};
+      kp.n = (int)p.hi_modes.size();
+      for (int k = 0; k < kp.n; ++k) {
+        const int m = p.hi_modes[k];
+        kp.ptr[k] = f.ptr[m];
+        kp.ext[k] = t.dims[m];
+        kp.valid[k] = t.dims[m];
+      }
+      krp_rows_kernel<<<sms * 8, 256, 0, stream>>>(kp, f.ld, p.Dq, width_ptr, width, buf, f.ld);
+    }
+    CALS_CUDA_TRY(cudaGetLastError());
+    hi = buf;
+  }
+
+  // tensor maps
+  auto key = std::make_pair(mode, variant);
+  std::unique_lock<std::mutex> maps_lock(t.mu);
+  auto it = t.amaps.find(key);
+  if (it == t.amaps.end()) {
+    CUtensorMap m;
+    int rc;
+    const int BM = ve.info.BM;
+    if (p.role == kRoleFirst)
+      rc = encode_map_3d(&m, t.data, p.D[0], p.D[1], p.D[2], BM + kPad, kBK, 1);
+    else if (p.role == kRoleMiddle)
+      rc = encode_map_3d(&m, t.data, p.D[0], p.D[1], p.D[2], kBK + kPad, BM, 1);
+    else
+      rc = encode_map_3d(&m, t.data, p.D[0], p.D[1], p.D[2], kBK + kPad, 1, BM);
+    if (rc) return rc;
+    it = t.amaps.emplace(key, m).first;
+  }
+  const CUtensorMap mapA = it->second;
+  maps_lock.unlock();
+  CUtensorMap mapB;
+  {
+    int rc = encode_map_2d(&mapB, lo, lo_ld, lrows, lo_ld, ve.info.BN + kPad, kBK);
+    if (rc) return rc;
+  }
+
+  MttkrpArgs a{};
+  a.role = p.role;
+  a.M = (int)p.M;
+  a.Dp = (int)p.Dp;
+  a.Dq = (int)p.Dq;
+  a.S = p.S;
+  a.width = width;
+  a.width_ptr = width_ptr;
+  a.hi = hi;
+  a.ldh = hi_ld;
+  a.out = p.S > 1 ? part : out;
+  a.ldo = p.S > 1 ? f.ld : ldo;
+  a.part_stride = (long long)p.M * f.ld;
+
+  const long long tm = (p.M + ve.info.BM - 1) / ve.info.BM;
+  const long long tn = (cap + ve.info.BN - 1) / ve.info.BN;
+  const long long units = tm * tn * p.S;
+  const long long slots = (long long)ve.occupancy() * sms;
+  dim3 grid((unsigned)std::max<long long>(1, std::min(units, slots)));
+  CALS_CUDA_TRY(ve.launch(grid, mapA, mapB, a, p.role != kRoleFirst, stream));
+  if (p.S > 1) {
+    const long long pairs = p.M * ((cap + 1) / 2);
+    const int blocks = (int)std::max<long long>(1, std::min<long long>(sms * 8, (pairs + 255) / 256));
+    split_reduce_kernel<<<blocks, 256, 0, stream>>>(part, a.part_stride, p.S, (int)p.M, f.ld,
+                                                    width_ptr, width, out, ldo);
+    CALS_CUDA_TRY(cudaGetLastError());
+  }
+  return kOk;
+}
+
+}  // namespace cals

@@ -1,0 +1,231 @@
+// Per-model ALS factor update on the block-diagonal structure of the fused
+// problem: Hadamard of the other modes' Gramians, upper Cholesky of the
+// R x R normal matrix, row-wise triangular solves, eigen-pinv fallback,
+// Gram refresh and the fast error / fit.  One thread block owns one model.
+//
+// Reference semantics restated (pkg/src/cals):
+//   hadamard_fold ascending, excluding mode n ......... driver.py:223-225, tensor.py:169-180
+//   update_factor: cho_factor(upper)+cho_solve, on
+//     LinAlgError / non-finite -> eigh pinv, cutoff
+//     1e-12 * max(lambda_max, 0); ValueError on
+//     non-finite input .................................. als.py:74-96
+//   gramian: upper triangle computed, lower mirrored .. tensor.py:183-188
+//   fast_error with the e > 0 ? e : 0 clamp ............ als.py:99-115
+//   fit = 1 - sqrt(e)/sqrt(||T||^2) ................... als.py:118-124
+#pragma once
+
+#include "common.cuh"
+
+namespace cals {
+
+constexpr int kUpdThreads = 128;
+
+// deterministic block sum (fixed tree); `red` has >= blockDim.x doubles
+__device__ __forceinline__ double block_sum(double v, double* red) {
+  red[threadIdx.x] = v;
+  __syncthreads();
+  for (int w = blockDim.x / 2; w > 0; w >>= 1) {
+    if (threadIdx.x < w) red[threadIdx.x] += red[threadIdx.x + w];
+    __syncthreads();
+  }
+  const double s = red[0];
+  __syncthreads();
+  return s;
+}
+
+// G = A^T A of the column block A[i][off + r] (rows x R, row stride ld):
+// upper triangle summed over ascending rows, then mirrored.
+__device__ inline void block_gram(const double* F, long long ld, int off, int rows, int R,
+                                  double* G) {
+  const int pairs = R * (R + 1) / 2;
+  for (int idx = threadIdx.x; idx < pairs; idx += blockDim.x) {
+    // decode idx -> (a, b), a <= b, row-major over the upper triangle
+    int a = 0, rem = idx;
+    while (rem >= R - a) {
+      rem -= R - a;
+      ++a;
+    }
+    const int b = a + rem;
+    const double* pa = F + off + a;
+    const double* pb = F + off + b;
+    double s = 0.0;
+    for (int i = 0; i < rows; ++i) s = fma(pa[(long long)i * ld], pb[(long long)i * ld], s);
+    G[a * R + b] = s;
+    G[b * R + a] = s;
+  }
+}
+
+// In-place upper Cholesky of the R x R matrix in shared memory (upper
+// triangle read and overwritten with U, H = U^T U).  Warp 0 factors; the
+// result flag is returned to every thread.  Fails like dpotrf: pivot <= 0
+// or NaN.
+__device__ inline bool block_cholesky_upper(double* H, int R, int* flag) {
+  if (threadIdx.x < 32) {
+    const int lane = threadIdx.x;
+    bool ok = true;
+    for (int j = 0; j < R && ok; ++j) {
+      const double d = H[j * R + j];
+      ok = d > 0.0;  // false for NaN
+      if (!ok) break;
+      const double u = sqrt(d);
+      __syncwarp();
+      if (lane == 0) H[j * R + j] = u;
+      for (int b = j + 1 + lane; b < R; b += 32) H[j * R + b] /= u;
+      __syncwarp();
+      for (int b = j + 1 + lane; b < R; b += 32) {
+        const double ujb = H[j * R + b];
+        for (int a = j + 1; a <= b; ++a) H[a * R + b] = fma(-H[j * R + a], ujb, H[a * R + b]);
+      }
+      __syncwarp();
+    }
+    if (lane == 0) *flag = ok ? 1 : 0;
+  }
+  __syncthreads();
+  return *flag != 0;
+}
+
+// Rows x = U^{-1} U^{-T} m for every row of the M block (dpotrs order:
+// forward with U^T, back with U).  X is shared scratch [R][nthr].  Writes the
+// solution into A; returns (block-wide) whether every entry is finite.
+__device__ inline bool block_row_solve(const double* U, int R, const double* Mb, long long ldm,
+                                       int rows, double* A, long long lda, double* X, int nthr) {
+  int bad = 0;
+  const int t = threadIdx.x;
+  if (t < nthr) {
+    for (int i = t; i < rows; i += nthr) {
+      const double* m = Mb + (long long)i * ldm;
+      for (int a = 0; a < R; ++a) X[a * nthr + t] = m[a];
+      for (int a = 0; a < R; ++a) {
+        double s = X[a * nthr + t];
+        for (int k = 0; k < a; ++k) s = fma(-U[k * R + a], X[k * nthr + t], s);
+        X[a * nthr + t] = s / U[a * R + a];
+      }
+      for (int a = R - 1; a >= 0; --a) {
+        double s = X[a * nthr + t];
+        for (int k = a + 1; k < R; ++k) s = fma(-U[a * R + k], X[k * nthr + t], s);
+        X[a * nthr + t] = s / U[a * R + a];
+      }
+      double* o = A + (long long)i * lda;
+      for (int a = 0; a < R; ++a) {
+        const double v = X[a * nthr + t];
+        bad |= !isfinite(v);
+        o[a] = v;
+      }
+    }
+  }
+  return __syncthreads_or(bad) == 0;
+}
+
+// Cyclic Jacobi eigen-decomposition of the symmetric R x R matrix H (full
+// storage), eigenvectors into V (columns).  Warp 0 only; cold path.
+__device__ inline void warp_jacobi(double* H, double* V, int R) {
+  const int lane = threadIdx.x & 31;
+  for (int idx = lane; idx < R * R; idx += 32) V[idx] = (idx / R == idx % R) ? 1.0 : 0.0;
+  __syncwarp();
+  for (int sweep = 0; sweep < 60; ++sweep) {
+    double off = 0.0, tot = 0.0;
+    for (int idx = lane; idx < R * R; idx += 32) {
+      const double v = H[idx] * H[idx];
+      tot += v;
+      if (idx / R != idx % R) off += v;
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+      off += __shfl_xor_sync(0xffffffffu, off, o);
+      tot += __shfl_xor_sync(0xffffffffu, tot, o);
+    }
+    if (off <= 1e-32 * tot || off == 0.0) break;
+    for (int p = 0; p < R - 1; ++p)
+      for (int q = p + 1; q < R; ++q) {
+        const double apq = H[p * R + q];
+        if (apq == 0.0) continue;
+        const double app = H[p * R + p], aqq = H[q * R + q];
+        const double theta = (aqq - app) / (2.0 * apq);
+        const double tt =
+            (theta >= 0 ? 1.0 : -1.0) / (fabs(theta) + sqrt(theta * theta + 1.0));
+        const double c = 1.0 / sqrt(tt * tt + 1.0), s = tt * c;
+        __syncwarp();
+        for (int k = lane; k < R; k += 32) {  // columns p, q
+          const double hkp = H[k * R + p], hkq = H[k * R + q];
+          H[k * R + p] = c * hkp - s * hkq;
+          H[k * R + q] = s * hkp + c * hkq;
+          const double vkp = V[k * R + p], vkq = V[k * R + q];
+          V[k * R + p] = c * vkp - s * vkq;
+          V[k * R + q] = s * vkp + c * vkq;
+        }
+        __syncwarp();
+        for (int k = lane; k < R; k += 32) {  // rows p, q
+          const double hpk = H[p * R + k], hqk = H[q * R + k];
+          H[p * R + k] = c * hpk - s * hqk;
+          H[q * R + k] = s * hpk + c * hqk;
+        }
+        __syncwarp();
+      }
+  }
+}
+
+// Pseudo-inverse fallback: H (smem, full symmetric, destroyed) -> P = pinv(H)
+// written into H; V and lam are scratch (R*R and R doubles).
+__device__ inline void block_pinv(double* H, double* V, double* lam, int R) {
+  if (threadIdx.x < 32) {
+    warp_jacobi(H, V, R);
+    __syncwarp();
+    if (threadIdx.x == 0) {
+      double lmax = -INFINITY;
+      for (int k = 0; k < R; ++k) {
+        lam[k] = H[k * R + k];
+        lmax = fmax(lmax, lam[k]);
+      }
+      const double cut = 1e-12 * fmax(lmax, 0.0);
+      for (int k = 0; k < R; ++k) lam[k] = lam[k] > cut ? 1.0 / lam[k] : 0.0;
+    }
+  }
+  __syncthreads();
+  for (int idx = threadIdx.x; idx < R * R; idx += blockDim.x) {
+    const int a = idx / R, b = idx % R;
+    double s = 0.0;
+    for (int k = 0; k < R; ++k) s = fma(V[a * R + k] * lam[k], V[b * R + k], s);
+    H[idx] = s;
+  }
+  __syncthreads();
+}
+
+// rows of A = m @ P
+__device__ inline void block_apply_pinv(const double* P, int R, const double* Mb, long long ldm,
+                                        int rows, double* A, long long lda) {
+  for (long long e = threadIdx.x; e < (long long)rows * R; e += blockDim.x) {
+    const int i = int(e / R), a = int(e % R);
+    const double* m = Mb + (long long)i * ldm;
+    double s = 0.0;
+    for (int b = 0; b < R; ++b) s = fma(m[b], P[b * R + a], s);
+    A[(long long)i * lda + a] = s;
+  }
+  __syncthreads();
+}
+
+// Full update of one column block: returns false if the inputs were
+// non-finite (the reference raises ValueError -> instance FAILED).
+// H (smem R*R) must hold the Hadamard product on entry; Hsave (R*R, any
+// memory) receives a copy for the pinv path; X/V/lam are scratch.
+__device__ inline bool block_update(double* H, double* Hsave, double* V, double* lam, double* X,
+                                    int nthr, int R, const double* Mb, long long ldm, int rows,
+                                    double* A, long long lda, int* flag) {
+  int bad = 0;
+  for (int idx = threadIdx.x; idx < R * R; idx += blockDim.x) {
+    bad |= !isfinite(H[idx]);
+    Hsave[idx] = H[idx];
+  }
+  for (long long e = threadIdx.x; e < (long long)rows * R; e += blockDim.x)
+    bad |= !isfinite(Mb[(e / R) * ldm + e % R]);
+  if (__syncthreads_or(bad)) return false;
+  bool ok = block_cholesky_upper(H, R, flag);
+  if (ok) ok = block_row_solve(H, R, Mb, ldm, rows, A, lda, X, nthr);
+  if (!ok) {
+    for (int idx = threadIdx.x; idx < R * R; idx += blockDim.x) H[idx] = Hsave[idx];
+    __syncthreads();
+    block_pinv(H, V, lam, R);
+    block_apply_pinv(H, R, Mb, ldm, rows, A, lda);
+  }
+  return true;
+}
+
+}  // namespace cals

@@ -1,0 +1,146 @@
+"""Python handle of the device-resident CALS engine (csrc/engine.cu).
+
+The engine owns, in HBM: the per-mode factor multi-matrices, Gramians,
+per-model status / fit bookkeeping, the FIFO queue and a model pool holding
+every model's starting (and finally its fitted) factors.  ``run`` replays a
+CUDA graph of one driver iteration until the device reports that every
+model has retired.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass
+from typing import Sequence
+
+import numpy as np
+
+from . import _native
+
+
+@dataclass
+class EngineResults:
+    pool: np.ndarray
+    status: np.ndarray
+    iterations: np.ndarray
+    error: np.ndarray
+    fit: np.ndarray
+    retire_seq: np.ndarray
+    seconds_active: np.ndarray
+    lambdas: np.ndarray
+
+
+class CalsEngine:
+    def __init__(self, dev_tensor, r_star: int, ranks: Sequence[int], trace_capacity: int = 4096):
+        _native.load()
+        self.dims = tuple(dev_tensor.dims)
+        self.order = len(self.dims)
+        self.ranks = np.asarray(ranks, dtype=np.int32)
+        self.r_star = int(r_star)
+        self.trace_capacity = int(trace_capacity)
+        self._tensor = dev_tensor  # keep alive
+        h = C.c_void_p()
+        _native.call("cals_engine_create", dev_tensor.handle, self.r_star, len(self.ranks),
+                     self.ranks.ctypes.data_as(C.POINTER(C.c_int32)), self.trace_capacity,
+                     C.byref(h))
+        self.handle = h
+        ptr, n = C.c_void_p(), C.c_int64()
+        _native.call("cals_engine_pool", h, C.byref(ptr), C.byref(n))
+        self.pool_ptr = ptr.value
+        self.pool_elems = n.value
+        # pool offsets (must match engine_create): model-major, modes ascending
+        self.offsets = np.zeros((len(self.ranks), self.order), dtype=np.int64)
+        at = 0
+        for k, r in enumerate(self.ranks):
+            for n_ in range(self.order):
+                self.offsets[k, n_] = at
+                at += self.dims[n_] * int(r)
+        assert at == self.pool_elems or (at == 0 and self.pool_elems == 0)
+
+    # -------------------------------------------------------------- pool
+    def pack(self, factor_lists) -> np.ndarray:
+        """Host pool: per model, per mode, row-major (I_n, R_k)."""
+        pool = np.empty(max(self.pool_elems, 1))
+        for k, facs in enumerate(factor_lists):
+            r = int(self.ranks[k])
+            for n_, f in enumerate(facs):
+                o = self.offsets[k, n_]
+                pool[o:o + self.dims[n_] * r] = np.ascontiguousarray(f, dtype=np.float64).ravel()
+        return pool[:self.pool_elems]
+
+    def unpack(self, pool: np.ndarray, k: int) -> list[np.ndarray]:
+        r = int(self.ranks[k])
+        out = []
+        for n_ in range(self.order):
+            o = self.offsets[k, n_]
+            out.append(np.asfortranarray(pool[o:o + self.dims[n_] * r].reshape(self.dims[n_], r)))
+        return out
+
+    def load_pool(self, pool, stream=None):
+        """``pool`` is a host ndarray or a CUDA tensor (device-to-device copy)."""
+        import torch
+
+        s = stream if stream is not None else torch.cuda.current_stream().cuda_stream
+        if isinstance(pool, np.ndarray):
+            pool = np.ascontiguousarray(pool, dtype=np.float64)
+            _native.call("cals_engine_load_pool", self.handle, pool.ctypes.data, 0, s)
+            torch.cuda.current_stream().synchronize()
+        else:
+            _native.call("cals_engine_load_pool", self.handle, C.c_void_p(pool.data_ptr()), 1, s)
+
+    # --------------------------------------------------------------- run
+    def run(self, tol: float, max_iterations: int, sqnorm: float, use_graph: bool = True,
+            stream=None) -> int:
+        import torch
+
+        s = stream if stream is not None else torch.cuda.current_stream().cuda_stream
+        it = C.c_int()
+        _native.call("cals_engine_run", self.handle, float(tol), int(max_iterations),
+                     float(sqnorm), 1 if use_graph else 0, s, C.byref(it))
+        return it.value
+
+    def results(self, with_pool: bool = True, stream=None) -> EngineResults:
+        import torch
+
+        s = stream if stream is not None else torch.cuda.current_stream().cuda_stream
+        k = len(self.ranks)
+        pool = np.empty(max(self.pool_elems, 1)) if with_pool else None
+        status = np.empty(k, np.int32)
+        iters = np.empty(k, np.int32)
+        err = np.empty(k)
+        fit = np.empty(k)
+        seq = np.empty(k, np.int32)
+        secs = np.empty(k)
+        lam = np.empty(max(int(self.ranks.sum()), 1))
+        ptr = (lambda a: None if a is None else a.ctypes.data)
+        _native.call("cals_engine_results", self.handle, ptr(pool), ptr(status), ptr(iters),
+                     ptr(err), ptr(fit), ptr(seq), ptr(secs), ptr(lam), s)
+        return EngineResults(pool, status, iters, err, fit, seq, secs, lam)
+
+    def trace(self):
+        cap = self.trace_capacity
+        w = np.empty(cap, np.int32)
+        a = np.empty(cap, np.int32)
+        sec = np.empty(cap)
+        cnt = C.c_int()
+        _native.call("cals_engine_trace", self.handle, w.ctypes.data, a.ctypes.data,
+                     sec.ctypes.data, cap, C.byref(cnt))
+        n = min(cnt.value, cap)
+        return [(int(w[i]), int(a[i]), float(sec[i])) for i in range(n)]
+
+    def variant(self, mode: int) -> dict:
+        v, bm, bn, s = C.c_int(), C.c_int(), C.c_int(), C.c_int()
+        _native.call("cals_engine_variant", self.handle, mode, C.byref(v), C.byref(bm),
+                     C.byref(bn), C.byref(s))
+        return {"variant": v.value, "BM": bm.value, "BN": bn.value, "splits": s.value}
+
+    def close(self):
+        if getattr(self, "handle", None):
+            _native.load(require_cuda=False).cals_engine_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass

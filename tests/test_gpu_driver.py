@@ -1,0 +1,161 @@
+"""GPU parity of the device-resident CALS driver through the public API.
+
+Bar (BASELINE.json north_star): factors within 1e-9 relative Frobenius after
+a fixed 5 iterations; fit within 1e-6 and equal iteration counts for
+converging runs; identical status / retirement order / trace widths.
+Compared with golden runs of the real reference and with the numpy oracle.
+"""
+import os
+
+import numpy as np
+import pytest
+
+from conftest import GOLDEN
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def cals():
+    import paper_2010_04678_b200 as c
+
+    c._native.load()
+    return c
+
+
+def rel(a, b):
+    return np.linalg.norm(np.asarray(a) - np.asarray(b)) / max(np.linalg.norm(b), 1.0)
+
+
+def _run_and_compare(cals, name, t, models, tol, iters, r_star, fac_tol=1e-9, fit_tol=1e-6):
+    g = np.load(os.path.join(GOLDEN, f"run_{name}.npz"))
+    trace = []
+    cfg = cals.ConvergenceConfig(tol=tol, max_iterations=iters)
+    out = cals.run(t, models, cfg, mode=cals.ExecutionMode.CALS, r_star=r_star, trace=trace)
+    assert [m.id for m in out] == [str(s) for s in g["order"]]
+    assert [m.status.value for m in out] == [str(s) for s in g["status"]]
+    assert [m.iterations_done for m in out] == g["iterations"].tolist()
+    assert [s.meta["width"] for s in trace] == g["widths"].tolist()
+    assert [s.meta["n_active"] for s in trace] == g["n_active"].tolist()
+    for m, f in zip(out, g["fit"]):
+        if np.isfinite(f):
+            assert abs(m.fit - f) <= fit_tol, (m.id, m.fit, f)
+    for m in out:
+        if f"{m.id}_f0" in g.files and m.status.value != "failed":
+            for n in range(t.order):
+                assert rel(m.factors[n], g[f"{m.id}_f{n}"]) <= fac_tol, (m.id, n)
+    return out
+
+
+def test_small_fixed_iterations(cals):
+    t = cals.generate_synthetic((12, 10, 8), 3, 0.1, seed=0)
+    ms = cals.build_models(t.dims, [1, 2, 3, 4], 2, seed=1)
+    _run_and_compare(cals, "small_fixed5", t, ms, 0.0, 5, sum(m.rank for m in ms))
+
+
+def test_small_refill_queue(cals):
+    t = cals.generate_synthetic((12, 10, 8), 3, 0.1, seed=0)
+    _run_and_compare(cals, "small_refill", t, cals.build_models(t.dims, [1, 2, 3, 4], 2, seed=1),
+                     1e-6, 200, 6, fac_tol=1e-6)
+
+
+def test_config1_fixed5_and_converging(cals):
+    t = cals.generate_synthetic((50, 50, 50), 5, 0.1, seed=0)
+    _run_and_compare(cals, "c1_fixed5", t, cals.build_models(t.dims, [1, 2, 3, 4, 5], 4, seed=1),
+                     0.0, 5, 60)
+    _run_and_compare(cals, "c1_tol", t, cals.build_models(t.dims, [1, 2, 3, 4, 5], 4, seed=1),
+                     1e-6, 1000, 60)
+
+
+def test_other_orders(cals):
+    t = cals.generate_synthetic((9, 7), 2, 0.05, seed=3)
+    _run_and_compare(cals, "order2", t, cals.build_models(t.dims, [1, 2, 3], 2, seed=4), 0.0, 6, 12)
+    t = cals.generate_synthetic((5, 4, 6, 3), 2, 0.05, seed=5)
+    _run_and_compare(cals, "order4", t, cals.build_models(t.dims, [1, 2, 3], 2, seed=6), 0.0, 6, 12)
+
+
+def test_failed_instance_isolated(cals):
+    f = np.load(os.path.join(GOLDEN, "fail_inputs.npz"))
+    t = cals.DenseTensor((4, 4, 3), f["data"])
+    good = cals.Model(id="good", rank=2, factors=[f[f"good_f{n}"] for n in range(3)])
+    bad = cals.Model(id="bad", rank=2, factors=[f[f"good_f{n}"] for n in range(3)])
+    for n in range(3):
+        bad.factors[n][...] = f[f"bad_f{n}"]  # plants the NaN post-validation
+    out = _run_and_compare(cals, "fail", t, [bad, good], 0.0, 3, 4)
+    by = {m.id: m for m in out}
+    assert by["bad"].status is cals.ModelStatus.FAILED
+    assert by["good"].status is cals.ModelStatus.ITERATION_CAP and by["good"].iterations_done == 3
+
+
+def test_cals_bitwise_equals_sequential(cals):
+    """test_driver.py:20-31: K=1 CALS == SEQUENTIAL bitwise (here: for every
+    model of a K>1 fused run -- the kernels are position-independent)."""
+    rng = np.random.default_rng(61)
+    t = cals.DenseTensor.from_array(rng.standard_normal((17, 13, 11)))
+    starts = [cals.Model.random(t.dims, r, rng, id=f"r{r}") for r in (1, 2, 3, 5, 8)]
+    cfg = cals.ConvergenceConfig(tol=0.0, max_iterations=10)
+    fused = {m.id: m for m in cals.run(t, starts, cfg, mode=cals.ExecutionMode.CALS, r_star=19)}
+    seq = {m.id: m for m in cals.run(t, starts, cfg, mode=cals.ExecutionMode.SEQUENTIAL)}
+    for k, m in fused.items():
+        assert m.error == seq[k].error and m.fit == seq[k].fit
+        for a, b in zip(m.factors, seq[k].factors):
+            assert np.array_equal(a, b)
+
+
+def test_inputs_not_mutated_and_capacity(cals):
+    rng = np.random.default_rng(68)
+    t = cals.DenseTensor.from_array(rng.standard_normal((5, 4, 3)))
+    starts = [cals.Model.random((5, 4, 3), 2, rng, id=f"m{i}") for i in range(2)]
+    snap = [[f.copy() for f in m.factors] for m in starts]
+    cals.run(t, starts, cals.ConvergenceConfig(tol=0.0, max_iterations=3), r_star=4)
+    for m, s in zip(starts, snap):
+        for a, b in zip(m.factors, s):
+            assert np.array_equal(a, b)
+    with pytest.raises(cals.CapacityError):
+        cals.run(t, [cals.Model.random((5, 4, 3), 3, rng, id="big")], cals.ConvergenceConfig(),
+                 r_star=2)
+
+
+def test_update_factor_golden(cals):
+    g = np.load(os.path.join(GOLDEN, "update.npz"))
+    for i in range(int(g["n_cases"])):
+        got = cals.update_factor(g[f"u{i}_m"], g[f"u{i}_h"])
+        want = g[f"u{i}_a"]
+        h = g[f"u{i}_h"]
+        if np.linalg.cond(h) < 1e10:
+            assert rel(got, want) <= 1e-10, i
+        else:  # singular: both must be the minimum-norm pinv solution
+            assert np.allclose(got, g[f"u{i}_m"] @ np.linalg.pinv(h), rtol=1e-9, atol=1e-9), i
+    assert cals.update_factor(np.array([[16.0], [20.0]]), np.array([[4.0]])).ravel().tolist() == [4.0, 5.0]
+    with pytest.raises(ValueError):
+        cals.update_factor(np.array([[np.nan, 0.0]]), np.eye(2))
+    with pytest.raises(ValueError):
+        cals.update_factor(np.ones((2, 2)), np.ones((2, 3)))
+
+
+def test_lambdas_are_column_norm_products(cals):
+    t = cals.generate_synthetic((12, 10, 8), 3, 0.1, seed=0)
+    out = cals.run(t, cals.build_models(t.dims, [2, 3], 1, seed=1),
+                   cals.ConvergenceConfig(tol=0.0, max_iterations=4), r_star=5)
+    for m in out:
+        want = np.prod([np.linalg.norm(f, axis=0) for f in m.factors], axis=0)
+        assert np.allclose(m.meta["lambdas"], want, rtol=1e-12)
+
+
+@pytest.mark.slow
+def test_eem_shape_refill_vs_oracle(cals):
+    """Config-3 shape (250x251x21) with converged-slot refill, reduced model
+    count so the CPU oracle finishes in seconds."""
+    from oracle import cals_oracle as O
+
+    dims, data = O.generate_synthetic((250, 251, 21), 10, 0.1, seed=0)
+    models = O.build_models(dims, [2, 4, 6, 8, 10], 2, seed=1)
+    ref = O.run_cals(data, dims, models, 1e-6, 300, 30)
+    t = cals.DenseTensor(dims, data)
+    ms = [cals.Model(id=i, rank=r, factors=[f.copy() for f in fac]) for i, r, fac in models]
+    out = cals.run(t, ms, cals.ConvergenceConfig(tol=1e-6, max_iterations=300), r_star=30)
+    assert [m.id for m in out] == [r.id for r in ref]
+    for m, r in zip(out, ref):
+        assert m.status.value == r.status
+        assert m.iterations_done == r.iterations
+        assert abs(m.fit - r.fit) <= 1e-6
