@@ -1,0 +1,346 @@
+"""Benchmark: models/sec of a full CALS sweep (BASELINE.json metric) on B200.
+
+Workload (BASELINE.json configs[1]): 200x200x200 synthetic
+tensor (generate_synthetic rank 20, noise 0.1, seed 0), 200 models = ranks
+1..20 x 10 random inits (build_models seed 1), r_star = 2100 (all admitted),
+a full sweep = every model run to retirement with tol = 0 and 5 iterations
+(the fixed-iteration sweep of BASELINE.md section 3).  A "step" is one such
+sweep.
+
+  value  -- device-resident: tensor + starting factors already in HBM, one
+            step = reload the model pool (D2D) + run the device loop to the
+            last retirement; CUDA events on the launch stream, L2 flushed
+            (256 MiB write) between steps, max over ranks.
+  e2e    -- the public API ``paper_2010_04678_b200.run`` with host numpy
+            inputs: fresh DenseTensor each step (tensor H2D), pool H2D,
+            results D2H, Model objects built -- wall clock with device syncs.
+  roofline -- the fused MTTKRP kernel (+ its split reduction) at the c2 shape
+            and W=2100 through cals_mttkrp, CUDA events; algorithmic flops =
+            2*W*prod(dims) per launch (mttkrp.py:72-76) against the FP64 DMMA
+            peak measured live by cals_fp64_peak_probe.
+  cpu_baseline -- the reference package (baseline/_ref, unmodified) on the
+            host cores: one CALS iteration of the same workload, extrapolated
+            to the 5-iteration sweep.
+
+Multi-GPU: one process per GPU (torchrun); each rank runs its own c2-sized
+model batch against a replicated tensor (no collective on the data path) ->
+"scaling": "weak".
+
+``--impl reference`` times the reference CPU implementation instead.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+DIMS = (200, 200, 200)
+RANKS = list(range(1, 21))
+PER_RANK = 10
+ITERS = 5
+R_STAR = 2100
+METRIC = "models/sec for full CALS sweep (200^3, 200 models, ranks 1-20 x 10, 5 iterations)"
+
+
+def _env_rank():
+    return (int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)),
+            int(os.environ.get("LOCAL_RANK", 0)))
+
+
+def _config(n_gpus: int, extra: dict | None = None) -> dict:
+    c = {"workload": "c2: 200x200x200 dense FP64, 200 CP models (ranks 1..20 x 10), "
+                     "tol=0, 5 iterations per model, r_star=2100",
+         "dims": list(DIMS), "models_per_gpu": len(RANKS) * PER_RANK, "iterations": ITERS,
+         "r_star": R_STAR, "parallelism": f"model-batch x{n_gpus}, tensor replicated",
+         "l2": "flushed between steps (256 MiB write)"}
+    if extra:
+        c.update(extra)
+    return c
+
+
+# ------------------------------------------------------------------ clocks --
+class ClockSampler:
+    def __init__(self, device: int):
+        self.device = device
+        self.samples = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def start(self):
+        self._t = threading.Thread(target=self._run, daemon=True)
+        self._t.start()
+        return self
+
+    def _run(self):
+        q = ("--query-gpu=clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+             "clocks_event_reasons.sw_power_cap")
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.device), q,
+                                      "--format=csv,noheader,nounits"], capture_output=True,
+                                     text=True, timeout=5).stdout.strip()
+                if out:
+                    self.samples.append([x.strip() for x in out.split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def stop(self) -> dict:
+        self._stop.set()
+        if self._t:
+            self._t.join(timeout=6)
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for s in self.samples for i in range(4)
+                          if len(s) > 2 + i and s[2 + i].lower() == "active"})
+        return {"sm_mhz": float(np.median(sm)) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+                "samples": len(self.samples)}
+
+
+# --------------------------------------------------------------- reference --
+def _reference_module():
+    """The unmodified reference package installed in baseline/_ref."""
+    path = os.path.join(ROOT, "baseline", "_ref")
+    if os.path.isdir(os.path.join(path, "cals")):
+        if path not in sys.path:
+            sys.path.insert(0, path)
+        import cals  # noqa: F401
+
+        return cals, "reference"
+    return None, "port"
+
+
+def cpu_sample(threads: int) -> dict:
+    """One CALS driver iteration of the c2 workload on the host cores."""
+    ref, kind = _reference_module()
+    if ref is not None:
+        from cals.als import ConvergenceConfig
+        from cals.driver import ExecutionMode, run
+        from cals.io import build_models, generate_synthetic
+
+        t = generate_synthetic(DIMS, 20, 0.1, seed=0)
+        models = build_models(DIMS, RANKS, PER_RANK, seed=1)
+        tic = time.perf_counter()
+        run(t, models, ConvergenceConfig(tol=0.0, max_iterations=1), mode=ExecutionMode.CALS,
+            r_star=R_STAR, threads=threads)
+        sec = time.perf_counter() - tic
+    else:
+        from oracle import cals_oracle as O
+
+        dims, data = O.generate_synthetic(DIMS, 20, 0.1, seed=0)
+        models = O.build_models(dims, RANKS, PER_RANK, seed=1)
+        tic = time.perf_counter()
+        O.run_cals(data, dims, models, 0.0, 1, R_STAR)
+        sec = time.perf_counter() - tic
+    n = len(RANKS) * PER_RANK
+    return {"value": n / (sec * ITERS), "unit": "models/s", "cores": threads, "kind": kind,
+            "sample": f"1 of {ITERS} CALS iterations over all {n} models (c2), "
+                      f"{sec:.2f} s, extrapolated x{ITERS}",
+            "seconds_per_iteration": sec}
+
+
+def run_reference_arm(args) -> None:
+    rank, world, _ = _env_rank()
+    if rank != 0:
+        return
+    threads = os.cpu_count() or 1
+    try:
+        from threadpoolctl import threadpool_limits
+    except Exception:  # pragma: no cover
+        threadpool_limits = None
+    times = []
+    for i in range(args.warmup + args.steps):
+        s = cpu_sample(threads)
+        if i >= args.warmup:
+            times.append(s["seconds_per_iteration"])
+    sec = float(np.mean(times)) * ITERS
+    n = len(RANKS) * PER_RANK
+    v = n / sec
+    line = {"impl": "reference", "metric": METRIC, "value": v, "unit": "models/s",
+            "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": sec * 1e3, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic (generate_synthetic seed 0)",
+            "config": _config(1, {"host": "reference CPU path, all host cores"}),
+            "cpu_baseline": {"value": v, "unit": "models/s", "cores": threads, "kind": s["kind"],
+                             "sample": s["sample"]},
+            "e2e": {"value": v, "unit": "models/s", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# --------------------------------------------------------------- our arm ---
+def main_gpu(args) -> None:
+    import ctypes as C
+
+    import torch
+    import torch.distributed as dist
+
+    import paper_2010_04678_b200 as cals
+    from paper_2010_04678_b200 import _native
+    from paper_2010_04678_b200.engine import CalsEngine
+
+    rank, world, local = _env_rank()
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    lib = _native.load()
+    stream = torch.cuda.current_stream()
+    s = stream.cuda_stream
+
+    t = cals.generate_synthetic(DIMS, 20, 0.1, seed=0)
+    models = cals.build_models(DIMS, RANKS, PER_RANK, seed=1 + rank)  # per-rank batch
+    n_models = len(models)
+    dev_t = t.device()
+    eng = CalsEngine(dev_t, R_STAR, [m.rank for m in models], trace_capacity=64)
+    pool_host = eng.pack([m.factors for m in models])
+    pool_dev = torch.from_numpy(pool_host).cuda()
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")
+    sq = t.sqnorm
+
+    def step():
+        eng.load_pool(pool_dev)
+        eng.run(0.0, ITERS, sq)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    clocks = ClockSampler(local).start()
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+          for _ in range(args.steps)]
+    torch.cuda.synchronize()
+    for i in range(args.steps):
+        flush.fill_(float(i))
+        ev[i][0].record(stream)
+        step()
+        ev[i][1].record(stream)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    ms = sum(a.elapsed_time(b) for a, b in ev) / args.steps
+    clk = clocks.stop()
+    res = eng.results(with_pool=False)
+    assert (res.iterations == ITERS).all() and (res.status == 3).all(), "sweep did not complete"
+    tmax = torch.tensor([ms], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(tmax, op=dist.ReduceOp.MAX)
+    ms_max = float(tmax.item())
+    value = n_models * world / (ms_max * 1e-3)
+    # launches per step: per iteration N x (mttkrp, reduce, update) + plan + move;
+    # plus the lookahead no-op iterations and the initial plan/move
+    iters_launched = ITERS + 3
+    gpu_launches = iters_launched * (3 * 3 + 2) + 2
+
+    # ---- e2e through the public API with host buffers
+    e2e_times = []
+    h2d = t.data.nbytes + pool_host.nbytes
+    d2h = pool_host.nbytes + n_models * (4 * 3 + 8 * 3) + 8 * sum(m.rank for m in models)
+    for i in range(args.warmup + max(2, min(args.steps, 5))):
+        tt = cals.DenseTensor(DIMS, t.data)  # fresh tensor: upload inside the timed region
+        torch.cuda.synchronize()
+        tic = time.perf_counter()
+        out = cals.run(tt, models, cals.ConvergenceConfig(tol=0.0, max_iterations=ITERS),
+                       r_star=R_STAR)
+        torch.cuda.synchronize()
+        if i >= args.warmup:
+            e2e_times.append(time.perf_counter() - tic)
+        tt.release_device()
+        assert len(out) == n_models
+    e2e_sec = float(np.mean(e2e_times))
+    te = torch.tensor([e2e_sec], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(te, op=dist.ReduceOp.MAX)
+    e2e = {"value": n_models * world / float(te.item()), "unit": "models/s",
+           "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h)}
+
+    # ---- roofline of the fused MTTKRP kernel at W = 2100
+    peak = C.c_double()
+    _native.call("cals_fp64_peak_probe", s, C.byref(peak))
+    W = R_STAR
+    fac = [torch.rand((d, W), dtype=torch.float64, device="cuda") for d in DIMS]
+    ptrs = (C.c_void_p * 3)(*[f.data_ptr() for f in fac])
+    out_t = torch.empty((max(DIMS), W), dtype=torch.float64, device="cuda")
+    per_mode = []
+    for n in range(3):
+        b = C.c_size_t()
+        _native.call("cals_mttkrp_workspace_bytes", dev_t.handle, n, W, C.byref(b))
+        work = torch.empty(b.value // 8 + 1, dtype=torch.float64, device="cuda")
+        args_ = (dev_t.handle, n, W, ptrs, W, out_t.data_ptr(), W, work.data_ptr(), b.value,
+                 eng.variant(n)["variant"], s)
+        for _ in range(2):
+            _native.call("cals_mttkrp", *args_)
+        reps = 5
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(reps):
+            _native.call("cals_mttkrp", *args_)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        per_mode.append(e0.elapsed_time(e1) / reps)
+    flops = 2.0 * W * np.prod(DIMS)
+    ach = flops / (np.mean(per_mode) * 1e-3) / 1e12
+    traffic = None
+    prof = os.path.join(ROOT, "profiles", "r01_mttkrp_ncu.json")
+    if os.path.exists(prof):
+        try:
+            traffic = json.load(open(prof)).get("dram_bytes_per_launch")
+        except Exception:
+            traffic = None
+    roofline = {"bound": "tensor", "achieved": ach, "peak": peak.value, "unit": "TFLOP/s",
+                "frac": ach / peak.value, "traffic": traffic,
+                "kernel": "mttkrp_dmma_kernel + split_reduce (cals_mttkrp), W=2100, c2 shape",
+                "ms_per_launch_by_mode": per_mode,
+                "peak_source": "cals_fp64_peak_probe: DMMA.8x8x4 all SMs, measured live "
+                               "(MEASURED_PEAKS.json has no FP64 entry)",
+                "flops_per_launch": flops}
+
+    line = {"metric": METRIC, "value": value, "unit": "models/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_max,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (generate_synthetic rank 20 noise 0.1 seed 0; build_models "
+                    "seed 1+rank)",
+            "config": _config(world, {"sweep_mttkrp_tflops": 3 * ITERS * 2 * sum(
+                m.rank for m in models) * np.prod(DIMS) / (ms_max * 1e-3) / 1e12}),
+            "clocks": clk, "e2e": e2e, "gpu_launches": gpu_launches, "roofline": roofline}
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        line["cpu_baseline"] = {k: v for k, v in cpu_sample(os.cpu_count() or 1).items()
+                                if k != "seconds_per_iteration"}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    eng.close()
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def main() -> None:
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        run_reference_arm(args)
+    else:
+        main_gpu(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -105,6 +105,11 @@ int cals_engine_trace(cals_engine* e, int32_t* widths, int32_t* n_active, double
                       int capacity, int* count);
 int cals_engine_variant(cals_engine* e, int mode, int* variant, int* bm, int* bn, int* splits);
 
+/* ---- diagnostics (no reference counterpart) ------------------------------
+ * Live FP64 tensor-core peak (DMMA.8x8x4 on every SM, TFLOP/s): the
+ * roofline denominator for the fused MTTKRP. */
+int cals_fp64_peak_probe(void* stream, double* tflops);
+
 #ifdef __cplusplus
 }
 #endif
