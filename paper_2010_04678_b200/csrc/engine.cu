@@ -79,6 +79,9 @@ struct EngState {
 };
 
 // ------------------------------------------------------------------ update --
+// RB > 0: fast path (every rank <= RB, rows in registers, chunked Gram);
+// RB == 0: generic path for ranks up to 128.  Same reference semantics.
+template <int RB>
 __global__ void __launch_bounds__(kUpdThreads) engine_update_kernel(EngState* st, int n,
                                                                      int nthr) {
   extern __shared__ __align__(16) double dsm[];
@@ -87,7 +90,7 @@ __global__ void __launch_bounds__(kUpdThreads) engine_update_kernel(EngState* st
   const int N = st->order;
   const int Rmax = st->max_rank;
   double* H = dsm;                // Rmax^2
-  double* X = H + Rmax * Rmax;    // Rmax * nthr
+  double* X = H + Rmax * Rmax;    // generic: Rmax * nthr; fast: kUpdThreads * (RB + 1)
   double* V = st->scratch + (long long)blockIdx.x * (2 * Rmax * Rmax + Rmax);
   double* Hsave = V + Rmax * Rmax;
   double* lam = Hsave + Rmax * Rmax;
@@ -104,12 +107,20 @@ __global__ void __launch_bounds__(kUpdThreads) engine_update_kernel(EngState* st
 
     if (n == 0 && st->fresh[k]) {
       // Gramians of the admitted starting point (driver.py:203-205)
-      for (int i = 1; i < N; ++i) block_gram(st->F[i], ld, off, (int)st->dims[i], R, gram(i));
+      for (int i = 1; i < N; ++i) {
+        if constexpr (RB > 0)
+          block_gram_fast<RB>(st->F[i] + off, ld, (int)st->dims[i], R, X, gram(i));
+        else
+          block_gram(st->F[i], ld, off, (int)st->dims[i], R, gram(i));
+      }
       __syncthreads();
       if (threadIdx.x == 0) st->fresh[k] = 0;
     }
     bool updated = false;
+    double inner = 0.0;
+    bool have_inner = false;
     if (!st->failed[k]) {
+      int bad = 0;
       for (int idx = threadIdx.x; idx < R * R; idx += blockDim.x) {
         double h = 1.0;
         bool first = true;
@@ -120,29 +131,48 @@ __global__ void __launch_bounds__(kUpdThreads) engine_update_kernel(EngState* st
           first = false;
         }
         H[idx] = h;
+        Hsave[idx] = h;
+        bad |= !isfinite(h);
       }
-      __syncthreads();
-      const bool finite_in = block_update(H, Hsave, V, lam, X, nthr, R, st->Mout + off, ld, rows,
-                                          st->F[n] + off, ld, &flag);
-      if (!finite_in) {
+      const double* Mb = st->Mout + off;
+      for (long long e = threadIdx.x; e < (long long)rows * R; e += blockDim.x)
+        bad |= !isfinite(Mb[(e / R) * ld + e % R]);
+      if (__syncthreads_or(bad)) {
+        // non-finite input: the reference raises ValueError -> FAILED (als.py:84-85)
         if (threadIdx.x == 0) st->failed[k] = 1;
+        __syncthreads();
       } else {
-        block_gram(st->F[n], ld, off, rows, R, gram(n));
+        bool done = false;
+        if constexpr (RB > 0) {
+          if (block_cholesky_upper(H, R, &flag)) {
+            done = block_solve_gram_fast<RB>(H, R, Mb, ld, rows, st->F[n] + off, ld, X, gram(n),
+                                             n == N - 1, &inner, red);
+            have_inner = done && n == N - 1;
+          }
+        }
+        if (!done) {
+          for (int idx = threadIdx.x; idx < R * R; idx += blockDim.x) H[idx] = Hsave[idx];
+          __syncthreads();
+          block_update(H, Hsave, V, lam, X, nthr, R, Mb, ld, rows, st->F[n] + off, ld, &flag);
+          block_gram(st->F[n], ld, off, rows, R, gram(n));
+        }
         updated = true;
       }
       __syncthreads();
     }
     if (n == N - 1) {
       // fast error / fit / stopping rule (driver.py:241-273, als.py:99-124)
-      double inner = 0.0, msq = 0.0;
+      double msq = 0.0;
       if (updated) {
-        double part = 0.0;
-        for (long long e = threadIdx.x; e < (long long)rows * R; e += blockDim.x) {
-          const long long i = e / R;
-          const int r = int(e % R);
-          part = fma(st->F[n][i * ld + off + r], st->Mout[i * ld + off + r], part);
+        if (!have_inner) {
+          double part = 0.0;
+          for (long long e = threadIdx.x; e < (long long)rows * R; e += blockDim.x) {
+            const long long i = e / R;
+            const int r = int(e % R);
+            part = fma(st->F[n][i * ld + off + r], st->Mout[i * ld + off + r], part);
+          }
+          inner = block_sum(part, red);
         }
-        inner = block_sum(part, red);
         double mpart = 0.0;
         for (int idx = threadIdx.x; idx < R * R; idx += blockDim.x) {
           double h = gram(0)[idx];
@@ -180,6 +210,15 @@ __global__ void __launch_bounds__(kUpdThreads) engine_update_kernel(EngState* st
       __syncthreads();
     }
   }
+}
+
+using UpdateKernel = void (*)(EngState*, int, int);
+static UpdateKernel update_kernel_for(int max_rank, int* rb) {
+  if (max_rank <= 8) { *rb = 8; return engine_update_kernel<8>; }
+  if (max_rank <= 16) { *rb = 16; return engine_update_kernel<16>; }
+  if (max_rank <= 32) { *rb = 32; return engine_update_kernel<32>; }
+  *rb = 0;
+  return engine_update_kernel<0>;
 }
 
 // -------------------------------------------------------------------- plan --
@@ -387,7 +426,8 @@ struct Engine {
   int* h_done = nullptr;  // mapped pinned
   int* d_done_alias = nullptr;
   int variants[kMaxOrder];
-  int upd_grid = 0, upd_nthr = 0;
+  int upd_grid = 0, upd_nthr = 0, upd_rb = 0;
+  UpdateKernel upd_kernel = nullptr;
   size_t upd_smem = 0, move_smem = 0;
   int move_grid = 0;
   cudaGraph_t graph = nullptr;
@@ -461,7 +501,9 @@ static int engine_create(Tensor* t, int capacity, int n_models, const int* ranks
   const int sms = sm_count(t->device);
   e->upd_grid = std::max(1, std::min(e->max_slots, sms * 4));
   e->upd_nthr = pick_nthr(rmax);
-  e->upd_smem = size_t(rmax) * rmax * 8 + size_t(rmax) * e->upd_nthr * 8;
+  e->upd_kernel = update_kernel_for(rmax, &e->upd_rb);
+  e->upd_smem = size_t(rmax) * rmax * 8 +
+                std::max(size_t(rmax) * e->upd_nthr, size_t(kUpdThreads) * (e->upd_rb + 1)) * 8;
   e->move_smem = size_t(e->ld) * 8;
   long long rows_total = 0, maxI = 1;
   for (int n = 0; n < N; ++n) {
@@ -469,7 +511,7 @@ static int engine_create(Tensor* t, int capacity, int n_models, const int* ranks
     maxI = std::max(maxI, t->dims[n]);
   }
   e->move_grid = (int)std::max<long long>(1, std::min<long long>(rows_total, sms * 8));
-  CALS_CUDA_TRY(cudaFuncSetAttribute(engine_update_kernel,
+  CALS_CUDA_TRY(cudaFuncSetAttribute(e->upd_kernel,
                                      cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      (int)e->upd_smem));
   CALS_CUDA_TRY(cudaFuncSetAttribute(engine_move_kernel,
@@ -602,8 +644,7 @@ static int enqueue_iteration(Engine* e, cudaStream_t stream) {
     int rc = launch_mttkrp(t, n, fs, 0, wptr, e->capacity, e->h_st.Mout, e->ld, e->d_ws,
                            e->ws_bytes, e->variants[n], stream);
     if (rc) return rc;
-    engine_update_kernel<<<e->upd_grid, kUpdThreads, e->upd_smem, stream>>>(e->d_st, n,
-                                                                            e->upd_nthr);
+    e->upd_kernel<<<e->upd_grid, kUpdThreads, e->upd_smem, stream>>>(e->d_st, n, e->upd_nthr);
     CALS_CUDA_TRY(cudaGetLastError());
   }
   engine_plan_kernel<<<1, 32, 0, stream>>>(e->d_st);

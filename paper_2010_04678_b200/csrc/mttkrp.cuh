@@ -68,6 +68,22 @@ struct TileCfg {
   static constexpr size_t kSmemBytes = STAGES * kStageBytes + 2 * STAGES * 8 + 128;
 };
 
+// p-tile `pt` loads the kBK-wide box at p0 and consumes its k4 steps
+// [ks_lo, ks_hi).  A ragged last tile is shifted left onto a multiple of 4 and
+// its already-consumed leading steps skipped, so no DMMA is spent on padding
+// beyond the last k4 group (Dp = 200 -> exactly 50 k4 steps).
+__device__ __forceinline__ void ptile(int pt, int Dp, int& p0, int& ks_lo, int& ks_hi) {
+  p0 = pt * kBK;
+  ks_lo = 0;
+  const int rem = Dp - p0;
+  if (rem < kBK && pt > 0) {
+    const int j = (kBK - rem) >> 2;
+    p0 -= 4 * j;
+    ks_lo = j;
+  }
+  ks_hi = min(kBK / 4, (Dp - p0 + 3) >> 2);
+}
+
 __device__ __forceinline__ void unit_decode(int u, int tm, int tn, int& tile_m, int& tile_n,
                                             int& s) {
   tile_n = u % tn;
@@ -125,7 +141,8 @@ __global__ void __launch_bounds__(TileCfg<MI, NI, WM, WN>::kThreads, 2)
             double* sa = smem + size_t(stage) * (C::A_ELEMS + C::B_ELEMS);
             double* sb = sa + C::A_ELEMS;
             mbar_arrive_expect_tx(&full[stage], stage_tx);
-            const int p0 = pt * kBK;
+            int p0, ks_lo, ks_hi;
+            ptile(pt, args.Dp, p0, ks_lo, ks_hi);
             if (args.role == kRoleFirst)
               tma_load_3d(sa, &tmA, &full[stage], m0, p0, q);
             else if (args.role == kRoleMiddle)
@@ -179,8 +196,11 @@ __global__ void __launch_bounds__(TileCfg<MI, NI, WM, WN>::kThreads, 2)
         mbar_wait(&full[stage], phase);
         const double* sa = smem + size_t(stage) * (C::A_ELEMS + C::B_ELEMS);
         const double* sb = sa + C::A_ELEMS;
+        int p0, ks_lo, ks_hi;
+        ptile(pt, args.Dp, p0, ks_lo, ks_hi);
 #pragma unroll
         for (int ks = 0; ks < kBK / 4; ++ks) {
+          if (ks < ks_lo || ks >= ks_hi) continue;
           const int k = 4 * ks + kq;
           double a[MI], b[NI];
           if constexpr (KC) {

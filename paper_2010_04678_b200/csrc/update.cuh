@@ -228,4 +228,138 @@ __device__ inline bool block_update(double* H, double* Hsave, double* V, double*
   return true;
 }
 
+// ---------------------------------------------------------------------------
+// Fast path for R <= RB (RB in {8, 16, 32}): one thread per factor row keeps
+// the row in registers; triangular solves in dpotrs/dtrsm order (forward:
+// for each a, subtract k ascending then divide; back: k descending), and the
+// Gram refresh accumulated from a shared-memory chunk of solved rows (pair
+// sums over rows in ascending order -> deterministic).
+
+template <int RB>
+struct FastPairs {
+  static constexpr int P = RB + 1;  // odd pitch: conflict-free row writes
+  static constexpr int NP = (RB * (RB + 1) / 2 + kUpdThreads - 1) / kUpdThreads;
+  int a[NP], b[NP];
+  double acc[NP];
+  __device__ void init(int R) {
+    const int npairs = R * (R + 1) / 2;
+#pragma unroll
+    for (int j = 0; j < NP; ++j) {
+      const int p = threadIdx.x + j * kUpdThreads;
+      acc[j] = 0.0;
+      a[j] = -1;
+      b[j] = -1;
+      if (p < npairs) {
+        int aa = 0, rem = p;
+        while (rem >= R - aa) {
+          rem -= R - aa;
+          ++aa;
+        }
+        a[j] = aa;
+        b[j] = aa + rem;
+      }
+    }
+  }
+  // rows [0, cnt) of the chunk Xs[row * P + col]
+  __device__ void accumulate(const double* Xs, int cnt) {
+#pragma unroll
+    for (int j = 0; j < NP; ++j) {
+      if (a[j] < 0) continue;
+      double s = acc[j];
+      const double* pa = Xs + a[j];
+      const double* pb = Xs + b[j];
+      for (int r = 0; r < cnt; ++r) s = fma(pa[r * P], pb[r * P], s);
+      acc[j] = s;
+    }
+  }
+  __device__ void store(double* G, int R) const {
+#pragma unroll
+    for (int j = 0; j < NP; ++j) {
+      if (a[j] < 0) continue;
+      G[a[j] * R + b[j]] = acc[j];
+      G[b[j] * R + a[j]] = acc[j];
+    }
+  }
+};
+
+// Gram of an existing column block (rows x R at F + off), chunked through Xs.
+template <int RB>
+__device__ inline void block_gram_fast(const double* F, long long ld, int rows, int R, double* Xs,
+                                       double* G) {
+  constexpr int P = FastPairs<RB>::P;
+  FastPairs<RB> pr;
+  pr.init(R);
+  for (int base = 0; base < rows; base += kUpdThreads) {
+    const int i = base + threadIdx.x;
+    if (i < rows) {
+      const double* row = F + (long long)i * ld;
+#pragma unroll
+      for (int a = 0; a < RB; ++a)
+        if (a < R) Xs[threadIdx.x * P + a] = row[a];
+    }
+    __syncthreads();
+    pr.accumulate(Xs, min(kUpdThreads, rows - base));
+    __syncthreads();
+  }
+  pr.store(G, R);
+}
+
+// Solve every row of the block against the upper Cholesky factor U (smem),
+// write A, refresh G = A^T A, and (want_inner) return sum(A o M).
+// Returns false when a solution entry is non-finite (caller -> pinv path).
+template <int RB>
+__device__ inline bool block_solve_gram_fast(const double* U, int R, const double* Mb, long long ldm,
+                                             int rows, double* A, long long lda, double* Xs,
+                                             double* G, bool want_inner, double* inner,
+                                             double* red) {
+  constexpr int P = FastPairs<RB>::P;
+  FastPairs<RB> pr;
+  pr.init(R);
+  double dot = 0.0;
+  int bad = 0;
+  for (int base = 0; base < rows; base += kUpdThreads) {
+    const int i = base + threadIdx.x;
+    if (i < rows) {
+      const double* m = Mb + (long long)i * ldm;
+      double x[RB];
+#pragma unroll
+      for (int a = 0; a < RB; ++a) x[a] = a < R ? m[a] : 0.0;
+#pragma unroll
+      for (int k = 0; k < RB; ++k) {
+        if (k < R) {
+          x[k] = x[k] / U[k * R + k];
+#pragma unroll
+          for (int a = k + 1; a < RB; ++a)
+            if (a < R) x[a] = fma(-U[k * R + a], x[k], x[a]);
+        }
+      }
+#pragma unroll
+      for (int k = RB - 1; k >= 0; --k) {
+        if (k < R) {
+          x[k] = x[k] / U[k * R + k];
+#pragma unroll
+          for (int a = 0; a < k; ++a) x[a] = fma(-U[a * R + k], x[k], x[a]);
+        }
+      }
+      double* o = A + (long long)i * lda;
+#pragma unroll
+      for (int a = 0; a < RB; ++a) {
+        if (a < R) {
+          bad |= !isfinite(x[a]);
+          o[a] = x[a];
+          Xs[threadIdx.x * P + a] = x[a];
+          if (want_inner) dot = fma(x[a], m[a], dot);
+        }
+      }
+    }
+    __syncthreads();
+    pr.accumulate(Xs, min(kUpdThreads, rows - base));
+    __syncthreads();
+  }
+  if (__syncthreads_or(bad)) return false;
+  pr.store(G, R);
+  if (want_inner) *inner = block_sum(dot, red);
+  return true;
+}
+
 }  // namespace cals
