@@ -135,8 +135,10 @@ __global__ void __launch_bounds__(kUpdThreads) engine_update_kernel(EngState* st
         bad |= !isfinite(h);
       }
       const double* Mb = st->Mout + off;
-      for (long long e = threadIdx.x; e < (long long)rows * R; e += blockDim.x)
-        bad |= !isfinite(Mb[(e / R) * ld + e % R]);
+      for (int i = threadIdx.x; i < rows; i += blockDim.x) {
+        const double* mrow = Mb + (long long)i * ld;
+        for (int a = 0; a < R; ++a) bad |= !isfinite(mrow[a]);
+      }
       if (__syncthreads_or(bad)) {
         // non-finite input: the reference raises ValueError -> FAILED (als.py:84-85)
         if (threadIdx.x == 0) st->failed[k] = 1;
@@ -144,9 +146,10 @@ __global__ void __launch_bounds__(kUpdThreads) engine_update_kernel(EngState* st
       } else {
         bool done = false;
         if constexpr (RB > 0) {
-          if (block_cholesky_upper(H, R, &flag)) {
-            done = block_solve_gram_fast<RB>(H, R, Mb, ld, rows, st->F[n] + off, ld, X, gram(n),
-                                             n == N - 1, &inner, red);
+          __shared__ double inv_diag[RB > 0 ? RB : 1];
+          if (warp_cholesky_reg<RB>(H, R, inv_diag, &flag)) {
+            done = block_solve_gram_fast<RB>(H, inv_diag, R, Mb, ld, rows, st->F[n] + off, ld, X,
+                                             gram(n), n == N - 1, &inner, red);
             have_inner = done && n == N - 1;
           }
         }
@@ -229,7 +232,7 @@ __global__ void engine_plan_kernel(EngState* st) {
   const int lane = threadIdx.x;
   const unsigned long long now = globaltimer_ns();
   const int n_old = st->n_active;
-  int new_n = 0, new_w = 0, retired = st->n_retired, moves = 0;
+  int new_n = 0, new_w = 0, retired = st->n_retired, moves = 0, pre = 0;
   for (int base = 0; base < n_old; base += 32) {
     const int s = base + lane;
     const bool valid = s < n_old;
@@ -246,6 +249,14 @@ __global__ void engine_plan_kernel(EngState* st) {
     const unsigned kmask = __ballot_sync(0xffffffffu, keep);
     const unsigned below = (1u << lane) - 1u;
     const int src = valid ? st->slot_off[s] : 0;
+    const int dst_keep = new_w + incl - rk;
+    const int ml = retiring ? st->rank[k] : (keep && dst_keep != src ? rk : 0);
+    int mincl = ml;
+    for (int o = 1; o < 32; o <<= 1) {
+      const int v = __shfl_up_sync(0xffffffffu, mincl, o);
+      if (lane >= o) mincl += v;
+    }
+    if (retiring || keep) st->mv_pre[moves + __popc((rmask | kmask) & below)] = pre + mincl - ml;
     if (retiring) {
       const int seq = retired + __popc(rmask & below);
       st->retire_seq[k] = seq;
@@ -277,6 +288,7 @@ __global__ void engine_plan_kernel(EngState* st) {
     new_n += __popc(kmask);
     retired += __popc(rmask);
     moves += __popc(rmask | kmask);
+    pre += __shfl_sync(0xffffffffu, mincl, 31);
   }
   if (lane == 0) {
     int head = st->queue_head;
@@ -292,14 +304,11 @@ __global__ void engine_plan_kernel(EngState* st) {
       st->mv_src[moves] = 0;
       st->mv_dst[moves] = new_w;
       st->mv_len[moves] = st->rank[k];
+      st->mv_pre[moves] = pre;
+      pre += st->rank[k];
       ++moves;
       ++new_n;
       new_w += st->rank[k];
-    }
-    int pre = 0;
-    for (int i = 0; i < moves; ++i) {
-      st->mv_pre[i] = pre;
-      pre += st->mv_len[i];
     }
     st->old_width = st->width;
     st->move_elems = pre;
@@ -408,6 +417,8 @@ static int pick_nthr(int R) {
   return nthr;
 }
 
+enum Tree : int { kTreeNone = 0, kTreeY = 1, kTreeZ = 2 };
+
 struct Engine {
   Tensor* t = nullptr;
   int order = 0, n_models = 0, capacity = 0, max_slots = 0, max_rank = 0;
@@ -426,6 +437,12 @@ struct Engine {
   int* h_done = nullptr;  // mapped pinned
   int* d_done_alias = nullptr;
   int variants[kMaxOrder];
+  // dimension tree (order 3): share one tensor-core contraction between two modes
+  int tree = 0;
+  ModePlan tree_plan;
+  int tree_variant = 0;
+  double* d_partial = nullptr;
+  double* d_ones = nullptr;
   int upd_grid = 0, upd_nthr = 0, upd_rb = 0;
   UpdateKernel upd_kernel = nullptr;
   size_t upd_smem = 0, move_smem = 0;
@@ -439,12 +456,61 @@ struct Engine {
 
 static size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
 
+// Dimension tree for 3-way tensors (ALS order 0,1,2):
+//   Y-tree: Y = X x_3 A2 is shared by modes 0 and 1 (A2 is not updated
+//           between them); mode 2 is a full fused MTTKRP.
+//   Z-tree: Z = X x_1 A0(new) is shared by modes 1 and 2 (A0 was updated
+//           before both); mode 0 is a full fused MTTKRP.
+// Two tensor-core contractions per iteration instead of three; the smaller
+// partial (I0*I1 vs I1*I2 rows) is chosen.  CALS_TREE=0|1|2 overrides.
+static int setup_tree(Engine* e) {
+  Tensor& t = *e->t;
+  e->tree = kTreeNone;
+  if (t.order != 3) return kOk;
+  const long long yrows = t.i0p * t.dims[1], zrows = t.dims[1] * t.dims[2];
+  int choice = yrows <= zrows ? kTreeY : kTreeZ;
+  if (const char* env = getenv("CALS_TREE")) choice = atoi(env);
+  if (choice != kTreeY && choice != kTreeZ) return kOk;
+  const long long rows = choice == kTreeY ? yrows : zrows;
+  const size_t bytes = size_t(rows) * size_t(e->ld) * 8;
+  size_t free_b = 0, total_b = 0;
+  CALS_CUDA_TRY(cudaMemGetInfo(&free_b, &total_b));
+  if (bytes > free_b / 2) return kOk;  // not worth starving the allocator
+  ModePlan& p = e->tree_plan;
+  p.S = 1;
+  p.Dq = 1;
+  if (choice == kTreeY) {
+    p.role = kRoleFirst;  // view (m = i + I0p j, p = k, q = 1)
+    p.D[0] = yrows;
+    p.D[1] = t.dims[2];
+    p.D[2] = 1;
+    p.M = yrows;
+    p.Dp = t.dims[2];
+  } else {
+    p.role = kRoleLast;   // view (p = i, q = 1, m = j + I1 k)
+    p.D[0] = t.i0p;
+    p.D[1] = 1;
+    p.D[2] = zrows;
+    p.M = zrows;
+    p.Dp = t.i0p;
+  }
+  CALS_CUDA_TRY(cudaMalloc(&e->d_partial, bytes));
+  CALS_CUDA_TRY(cudaMalloc(&e->d_ones, size_t(e->ld) * 8));
+  std::vector<double> ones(e->ld, 1.0);
+  CALS_CUDA_TRY(cudaMemcpy(e->d_ones, ones.data(), size_t(e->ld) * 8, cudaMemcpyHostToDevice));
+  e->tree_variant = choose_variant(p.M, e->capacity, 1);
+  e->tree = choice;
+  return kOk;
+}
+
 static int engine_free(Engine* e) {
   if (!e) return kOk;
   if (e->exec) cudaGraphExecDestroy(e->exec);
   if (e->graph) cudaGraphDestroy(e->graph);
   if (e->d_block) cudaFree(e->d_block);
   if (e->d_ws) cudaFree(e->d_ws);
+  if (e->d_partial) cudaFree(e->d_partial);
+  if (e->d_ones) cudaFree(e->d_ones);
   if (e->d_st) cudaFree(e->d_st);
   if (e->h_done) cudaFreeHost(e->h_done);
   delete e;
@@ -604,6 +670,8 @@ static int engine_create(Tensor* t, int capacity, int n_models, const int* ranks
     e->variants[n] = choose_variant(t->plans[n].M, capacity, t->plans[n].S);
   }
   CALS_CUDA_TRY(cudaMalloc(&e->d_ws, e->ws_bytes));
+  int rc = setup_tree(e.get());
+  if (rc) return rc;
   *out = e.release();
   return kOk;
 }
@@ -640,9 +708,38 @@ static int enqueue_iteration(Engine* e, cudaStream_t stream) {
   for (int n = 0; n < N; ++n) fs.ptr[n] = e->h_st.F[n];
   fs.ld = e->ld;
   const int* wptr = &e->d_st->width;
+  const int sms = sm_count(t.device);
+  double* const* F = e->h_st.F;
+  double* Mo = e->h_st.Mout;
+  const long long ld = e->ld, cap = e->capacity;
   for (int n = 0; n < N; ++n) {
-    int rc = launch_mttkrp(t, n, fs, 0, wptr, e->capacity, e->h_st.Mout, e->ld, e->d_ws,
-                           e->ws_bytes, e->variants[n], stream);
+    int rc = kOk;
+    if (e->tree == kTreeY && n == 0) {
+      // Y[i + I0p j][c] = sum_k X[i,j,k] A2[k][c]  (tensor cores), then M0 = Y x_j A1
+      rc = launch_contraction(t, e->tree_plan, 100, F[2], t.dims[2], ld, e->d_ones, ld, 0, wptr,
+                              cap, e->d_partial, ld, nullptr, e->tree_variant, stream);
+      if (!rc)
+        rc = launch_partial_ttv(e->d_partial, ld, t.i0p, t.dims[1], 1, t.dims[0], F[1], ld, 0,
+                                wptr, cap, t.dims[0], Mo, ld, sms, stream);
+    } else if (e->tree == kTreeY && n == 1) {
+      // M1 = Y x_i A0(new): A2 unchanged since Y was formed
+      rc = launch_partial_ttv(e->d_partial, ld, t.i0p, t.dims[1], 0, t.dims[0], F[0], ld, 0,
+                              wptr, cap, t.dims[1], Mo, ld, sms, stream);
+    } else if (e->tree == kTreeZ && n == 1) {
+      // Z[j + I1 k][c] = sum_i X[i,j,k] A0(new)[i][c], then M1 = Z x_k A2
+      rc = launch_contraction(t, e->tree_plan, 101, F[0], t.dims[0], ld, e->d_ones, ld, 0, wptr,
+                              cap, e->d_partial, ld, nullptr, e->tree_variant, stream);
+      if (!rc)
+        rc = launch_partial_ttv(e->d_partial, ld, t.dims[1], t.dims[2], 1, t.dims[1], F[2], ld, 0,
+                                wptr, cap, t.dims[1], Mo, ld, sms, stream);
+    } else if (e->tree == kTreeZ && n == 2) {
+      // M2 = Z x_j A1(new): A0 unchanged since Z was formed
+      rc = launch_partial_ttv(e->d_partial, ld, t.dims[1], t.dims[2], 0, t.dims[1], F[1], ld, 0,
+                              wptr, cap, t.dims[2], Mo, ld, sms, stream);
+    } else {
+      rc = launch_mttkrp(t, n, fs, 0, wptr, cap, Mo, ld, e->d_ws, e->ws_bytes, e->variants[n],
+                         stream);
+    }
     if (rc) return rc;
     e->upd_kernel<<<e->upd_grid, kUpdThreads, e->upd_smem, stream>>>(e->d_st, n, e->upd_nthr);
     CALS_CUDA_TRY(cudaGetLastError());

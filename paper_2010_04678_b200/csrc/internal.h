@@ -80,6 +80,23 @@ int launch_mttkrp(Tensor& t, int mode, const FactorSet& f, int width, const int*
                   long long cap, double* out, long long ldo, double* workspace,
                   size_t workspace_bytes, int variant, cudaStream_t stream);
 
+// Lower level: one contraction on an arbitrary 3-D view plan `p` of the tensor
+// with explicit Lo [lrows][lo_ld] / Hi [Dq][hi_ld] operands.  map_key caches
+// the tensor map (modes use their index, engine-private plans use >= 100).
+// S > 1 needs `part` (S * M * lo_ld doubles) and reduces into `out`.
+int launch_contraction(Tensor& t, const ModePlan& p, int map_key, const double* lo,
+                       long long lrows, long long lo_ld, const double* hi, long long hi_ld,
+                       int width, const int* width_ptr, long long cap, double* out, long long ldo,
+                       double* part, int variant, cudaStream_t stream);
+
+// out[row][c] = sum over the reduced index of P[a + Da*b][c] * F[idx][c]
+// (reduce_b: rows a < rows_out, sum b < Db with F[b]; else rows b, sum a < La
+// with F[a]).  Deterministic ascending order; memory-bound.
+int launch_partial_ttv(const double* P, long long ld, long long Da, long long Db, int reduce_b,
+                       long long La, const double* F, long long ldf, int width,
+                       const int* width_ptr, long long cap, long long rows_out, double* out,
+                       long long ldo, int sms, cudaStream_t stream);
+
 // Tensor maps ------------------------------------------------------------------
 int encode_map_2d(CUtensorMap* m, const double* base, long long inner, long long outer,
                   long long ld_elems, int box_inner, int box_outer);

@@ -401,8 +401,6 @@ int launch_mttkrp(Tensor& t, int mode, const FactorSet& f, int width, const int*
              "width must be in [1, capacity]");
   CALS_CHECK(mttkrp_workspace_bytes(t, mode, f.ld) <= workspace_bytes || p.S == 1, kErrInvalid,
              "MTTKRP workspace too small");
-  if (variant < 0) variant = choose_variant(p.M, cap, p.S);
-  const VariantEntry& ve = kVariants[variant];
   const int sms = sm_count(t.device);
 
   // carve the workspace
@@ -455,9 +453,20 @@ int launch_mttkrp(Tensor& t, int mode, const FactorSet& f, int width, const int*
     CALS_CUDA_TRY(cudaGetLastError());
     hi = buf;
   }
+  return launch_contraction(t, p, mode, lo, lrows, lo_ld, hi, hi_ld, width, width_ptr, cap, out,
+                            ldo, part, variant, stream);
+}
 
+int launch_contraction(Tensor& t, const ModePlan& p, int map_key, const double* lo,
+                       long long lrows, long long lo_ld, const double* hi, long long hi_ld,
+                       int width, const int* width_ptr, long long cap, double* out, long long ldo,
+                       double* part, int variant, cudaStream_t stream) {
+  if (variant < 0) variant = choose_variant(p.M, cap, p.S);
+  const VariantEntry& ve = kVariants[variant];
+  const int sms = sm_count(t.device);
+  CALS_CHECK(p.S == 1 || part != nullptr, kErrInvalid, "split-K needs a partial buffer");
   // tensor maps
-  auto key = std::make_pair(mode, variant);
+  auto key = std::make_pair(map_key, variant);
   std::unique_lock<std::mutex> maps_lock(t.mu);
   auto it = t.amaps.find(key);
   if (it == t.amaps.end()) {
@@ -492,8 +501,8 @@ int launch_mttkrp(Tensor& t, int mode, const FactorSet& f, int width, const int*
   a.hi = hi;
   a.ldh = hi_ld;
   a.out = p.S > 1 ? part : out;
-  a.ldo = p.S > 1 ? f.ld : ldo;
-  a.part_stride = (long long)p.M * f.ld;
+  a.ldo = p.S > 1 ? lo_ld : ldo;
+  a.part_stride = (long long)p.M * lo_ld;
 
   const long long tm = (p.M + ve.info.BM - 1) / ve.info.BM;
   const long long tn = (cap + ve.info.BN - 1) / ve.info.BN;
@@ -504,10 +513,68 @@ int launch_mttkrp(Tensor& t, int mode, const FactorSet& f, int width, const int*
   if (p.S > 1) {
     const long long pairs = p.M * ((cap + 1) / 2);
     const int blocks = (int)std::max<long long>(1, std::min<long long>(sms * 8, (pairs + 255) / 256));
-    split_reduce_kernel<<<blocks, 256, 0, stream>>>(part, a.part_stride, p.S, (int)p.M, f.ld,
+    split_reduce_kernel<<<blocks, 256, 0, stream>>>(part, a.part_stride, p.S, (int)p.M, lo_ld,
                                                     width_ptr, width, out, ldo);
     CALS_CUDA_TRY(cudaGetLastError());
   }
+  return kOk;
+}
+
+// ------------------------------------------------- dimension-tree partials --
+// Second half of a dimension-tree MTTKRP: the partial P (one tensor mode
+// already contracted on the tensor cores) is contracted with one more factor
+// column-wise.  Thread per (row, c), c fastest -> coalesced 8-byte loads of P
+// and F; the reduction runs in ascending index order (deterministic,
+// column-local, so position independence is preserved).
+__global__ void partial_ttv_kernel(const double* __restrict__ P, long long ld, long long Da,
+                                   long long Db, int reduce_b, long long La,
+                                   const double* __restrict__ F, long long ldf,
+                                   const int* width_ptr, int width, long long rows_out,
+                                   double* __restrict__ out, long long ldo) {
+  const int W = width_ptr ? *width_ptr : width;
+  const long long n = rows_out * W;
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < n;
+       e += (long long)gridDim.x * blockDim.x) {
+    const long long row = e / W;
+    const int c = int(e % W);
+    const double* p;
+    const double* f = F + c;
+    long long pstep, L;
+    if (reduce_b) {  // out[a] = sum_b P[a + Da b] F[b]
+      p = P + row * ld + c;
+      pstep = Da * ld;
+      L = Db;
+    } else {         // out[b] = sum_a P[a + Da b] F[a]
+      p = P + row * Da * ld + c;
+      pstep = ld;
+      L = La;
+    }
+    double acc = 0.0;
+    long long i = 0;
+    for (; i + 4 <= L; i += 4) {
+      const double p0 = __ldg(p + (i + 0) * pstep), p1 = __ldg(p + (i + 1) * pstep);
+      const double p2 = __ldg(p + (i + 2) * pstep), p3 = __ldg(p + (i + 3) * pstep);
+      const double f0 = __ldg(f + (i + 0) * ldf), f1 = __ldg(f + (i + 1) * ldf);
+      const double f2 = __ldg(f + (i + 2) * ldf), f3 = __ldg(f + (i + 3) * ldf);
+      acc = fma(p0, f0, acc);
+      acc = fma(p1, f1, acc);
+      acc = fma(p2, f2, acc);
+      acc = fma(p3, f3, acc);
+    }
+    for (; i < L; ++i) acc = fma(__ldg(p + i * pstep), __ldg(f + i * ldf), acc);
+    out[row * ldo + c] = acc;
+  }
+}
+
+int launch_partial_ttv(const double* P, long long ld, long long Da, long long Db, int reduce_b,
+                       long long La, const double* F, long long ldf, int width,
+                       const int* width_ptr, long long cap, long long rows_out, double* out,
+                       long long ldo, int sms, cudaStream_t stream) {
+  const long long n = rows_out * cap;
+  const int blocks = (int)std::max<long long>(1, std::min<long long>(sms * 16, (n + 255) / 256));
+  partial_ttv_kernel<<<blocks, 256, 0, stream>>>(P, ld, Da, Db, reduce_b, La, F, ldf, width_ptr,
+                                                 width, rows_out, out, ldo);
+  CALS_CUDA_TRY(cudaGetLastError());
   return kOk;
 }
 

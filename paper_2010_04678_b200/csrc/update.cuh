@@ -282,6 +282,52 @@ struct FastPairs {
   }
 };
 
+// Register-resident upper Cholesky by warp 0 for R <= RB <= 32: lane b holds
+// column b of H; step k broadcasts the pivot and row k with shuffles, so the
+// only serial chain is one sqrt + one divide per step.  Writes U into the
+// upper triangle of H and 1/U[k][k] into inv_diag (the row solves multiply by
+// the reciprocal, as OpenBLAS's packed trsm kernels do).  Fails like dpotrf.
+template <int RB>
+__device__ inline bool warp_cholesky_reg(double* H, int R, double* inv_diag, int* flag) {
+  if (threadIdx.x < 32) {
+    const int lane = threadIdx.x;
+    double c[RB];
+#pragma unroll
+    for (int a = 0; a < RB; ++a) c[a] = (a < R && lane < R) ? H[a * R + lane] : 0.0;
+    bool ok = true;
+#pragma unroll
+    for (int k = 0; k < RB; ++k) {
+      if (k < R && ok) {
+        const double piv = __shfl_sync(0xffffffffu, c[k], k);
+        if (!(piv > 0.0)) {
+          ok = false;
+        } else {
+          const double u = sqrt(piv);
+          if (lane == k) {
+            c[k] = u;
+            inv_diag[k] = 1.0 / u;
+          } else if (lane > k) {
+            c[k] = c[k] / u;
+          }
+#pragma unroll
+          for (int a = k + 1; a < RB; ++a) {
+            const double uka = __shfl_sync(0xffffffffu, c[k], a);
+            if (a < R && lane >= a) c[a] = fma(-uka, c[k], c[a]);
+          }
+        }
+      }
+    }
+    if (ok && lane < R) {
+#pragma unroll
+      for (int a = 0; a < RB; ++a)
+        if (a <= lane) H[a * R + lane] = c[a];
+    }
+    if (lane == 0) *flag = ok ? 1 : 0;
+  }
+  __syncthreads();
+  return *flag != 0;
+}
+
 // Gram of an existing column block (rows x R at F + off), chunked through Xs.
 template <int RB>
 __device__ inline void block_gram_fast(const double* F, long long ld, int rows, int R, double* Xs,
@@ -308,7 +354,7 @@ __device__ inline void block_gram_fast(const double* F, long long ld, int rows, 
 // write A, refresh G = A^T A, and (want_inner) return sum(A o M).
 // Returns false when a solution entry is non-finite (caller -> pinv path).
 template <int RB>
-__device__ inline bool block_solve_gram_fast(const double* U, int R, const double* Mb, long long ldm,
+__device__ inline bool block_solve_gram_fast(const double* U, const double* inv_diag, int R, const double* Mb, long long ldm,
                                              int rows, double* A, long long lda, double* Xs,
                                              double* G, bool want_inner, double* inner,
                                              double* red) {
@@ -327,7 +373,7 @@ __device__ inline bool block_solve_gram_fast(const double* U, int R, const doubl
 #pragma unroll
       for (int k = 0; k < RB; ++k) {
         if (k < R) {
-          x[k] = x[k] / U[k * R + k];
+          x[k] = x[k] * inv_diag[k];
 #pragma unroll
           for (int a = k + 1; a < RB; ++a)
             if (a < R) x[a] = fma(-U[k * R + a], x[k], x[a]);
@@ -336,7 +382,7 @@ __device__ inline bool block_solve_gram_fast(const double* U, int R, const doubl
 #pragma unroll
       for (int k = RB - 1; k >= 0; --k) {
         if (k < R) {
-          x[k] = x[k] / U[k * R + k];
+          x[k] = x[k] * inv_diag[k];
 #pragma unroll
           for (int a = 0; a < k; ++a) x[a] = fma(-U[a * R + k], x[k], x[a]);
         }

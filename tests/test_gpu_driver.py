@@ -159,3 +159,16 @@ def test_eem_shape_refill_vs_oracle(cals):
         assert m.status.value == r.status
         assert m.iterations_done == r.iterations
         assert abs(m.fit - r.fit) <= 1e-6
+
+
+@pytest.mark.parametrize("tree", ["0", "1", "2"])
+def test_dimension_tree_variants_match_reference(cals, tree, monkeypatch):
+    """The engine's dimension-tree schedules (none / Y = X x3 A2 shared by
+    modes 0,1 / Z = X x1 A0 shared by modes 1,2) all meet the parity bar."""
+    monkeypatch.setenv("CALS_TREE", tree)
+    t = cals.generate_synthetic((50, 50, 50), 5, 0.1, seed=0)
+    _run_and_compare(cals, "c1_fixed5", t, cals.build_models(t.dims, [1, 2, 3, 4, 5], 4, seed=1),
+                     0.0, 5, 60)
+    t = cals.generate_synthetic((12, 10, 8), 3, 0.1, seed=0)
+    _run_and_compare(cals, "small_refill", t, cals.build_models(t.dims, [1, 2, 3, 4], 2, seed=1),
+                     1e-6, 200, 6, fac_tol=1e-6)
