@@ -477,28 +477,23 @@ static int setup_tree(Engine* e) {
   CALS_CUDA_TRY(cudaMemGetInfo(&free_b, &total_b));
   if (bytes > free_b / 2) return kOk;  // not worth starving the allocator
   ModePlan& p = e->tree_plan;
-  p.S = 1;
-  p.Dq = 1;
   if (choice == kTreeY) {
-    p.role = kRoleFirst;  // view (m = i + I0p j, p = k, q = 1)
-    p.D[0] = yrows;
-    p.D[1] = t.dims[2];
-    p.D[2] = 1;
-    p.M = yrows;
+    // mode 0 as view (m = i, q = j, p = k): the tensor cores contract k, so
+    // each per-slab product is Y[i, j, :] -- written once as a side output
+    // while the same kernel scales by A1[j] and accumulates M0.
+    p = t.plans[0];
+    p.role = kRoleFirstQP;
     p.Dp = t.dims[2];
+    p.Dq = t.dims[1];
+    p.S = (int)std::min<long long>(p.Dq, 32);
+    p.lo_modes = {2};
+    p.hi_modes = {1};
   } else {
-    p.role = kRoleLast;   // view (p = i, q = 1, m = j + I1 k)
-    p.D[0] = t.i0p;
-    p.D[1] = 1;
-    p.D[2] = zrows;
-    p.M = zrows;
-    p.Dp = t.i0p;
+    p = t.plans[1];  // MIDDLE: slab product over q = k is Z[j, k, :]
   }
+  e->ws_bytes = std::max(e->ws_bytes, size_t(p.S) * size_t(p.M) * size_t(e->ld) * 8 + 256);
   CALS_CUDA_TRY(cudaMalloc(&e->d_partial, bytes));
-  CALS_CUDA_TRY(cudaMalloc(&e->d_ones, size_t(e->ld) * 8));
-  std::vector<double> ones(e->ld, 1.0);
-  CALS_CUDA_TRY(cudaMemcpy(e->d_ones, ones.data(), size_t(e->ld) * 8, cudaMemcpyHostToDevice));
-  e->tree_variant = choose_variant(p.M, e->capacity, 1);
+  e->tree_variant = choose_variant(p.M, e->capacity, p.S);
   e->tree = choice;
   return kOk;
 }
@@ -669,9 +664,9 @@ static int engine_create(Tensor* t, int capacity, int n_models, const int* ranks
     e->ws_bytes = std::max(e->ws_bytes, mttkrp_workspace_bytes(*t, n, e->ld));
     e->variants[n] = choose_variant(t->plans[n].M, capacity, t->plans[n].S);
   }
-  CALS_CUDA_TRY(cudaMalloc(&e->d_ws, e->ws_bytes));
   int rc = setup_tree(e.get());
   if (rc) return rc;
+  CALS_CUDA_TRY(cudaMalloc(&e->d_ws, e->ws_bytes));
   *out = e.release();
   return kOk;
 }
@@ -715,23 +710,18 @@ static int enqueue_iteration(Engine* e, cudaStream_t stream) {
   for (int n = 0; n < N; ++n) {
     int rc = kOk;
     if (e->tree == kTreeY && n == 0) {
-      // Y[i + I0p j][c] = sum_k X[i,j,k] A2[k][c]  (tensor cores), then M0 = Y x_j A1
-      rc = launch_contraction(t, e->tree_plan, 100, F[2], t.dims[2], ld, e->d_ones, ld, 0, wptr,
-                              cap, e->d_partial, ld, nullptr, e->tree_variant, stream);
-      if (!rc)
-        rc = launch_partial_ttv(e->d_partial, ld, t.i0p, t.dims[1], 1, t.dims[0], F[1], ld, 0,
-                                wptr, cap, t.dims[0], Mo, ld, sms, stream);
+      // M0 = sum_j A1[j] (sum_k X[:,j,k] A2[k]); the inner slab products are
+      // the partial Y[i + I0p j] kept for mode 1
+      rc = launch_contraction(t, e->tree_plan, 100, F[2], t.dims[2], ld, F[1], ld, 0, wptr, cap,
+                              Mo, ld, e->d_ws, e->tree_variant, stream, e->d_partial, ld, t.i0p);
     } else if (e->tree == kTreeY && n == 1) {
       // M1 = Y x_i A0(new): A2 unchanged since Y was formed
       rc = launch_partial_ttv(e->d_partial, ld, t.i0p, t.dims[1], 0, t.dims[0], F[0], ld, 0,
                               wptr, cap, t.dims[1], Mo, ld, sms, stream);
     } else if (e->tree == kTreeZ && n == 1) {
-      // Z[j + I1 k][c] = sum_i X[i,j,k] A0(new)[i][c], then M1 = Z x_k A2
-      rc = launch_contraction(t, e->tree_plan, 101, F[0], t.dims[0], ld, e->d_ones, ld, 0, wptr,
-                              cap, e->d_partial, ld, nullptr, e->tree_variant, stream);
-      if (!rc)
-        rc = launch_partial_ttv(e->d_partial, ld, t.dims[1], t.dims[2], 1, t.dims[1], F[2], ld, 0,
-                                wptr, cap, t.dims[1], Mo, ld, sms, stream);
+      // M1 = sum_k A2[k] (sum_i X[i,:,k] A0(new)[i]); slab products = Z[j + I1 k]
+      rc = launch_contraction(t, e->tree_plan, 1, F[0], t.dims[0], ld, F[2], ld, 0, wptr, cap, Mo,
+                              ld, e->d_ws, e->tree_variant, stream, e->d_partial, ld, t.dims[1]);
     } else if (e->tree == kTreeZ && n == 2) {
       // M2 = Z x_j A1(new): A0 unchanged since Z was formed
       rc = launch_partial_ttv(e->d_partial, ld, t.dims[1], t.dims[2], 0, t.dims[1], F[1], ld, 0,

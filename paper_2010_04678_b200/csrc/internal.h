@@ -87,7 +87,8 @@ int launch_mttkrp(Tensor& t, int mode, const FactorSet& f, int width, const int*
 int launch_contraction(Tensor& t, const ModePlan& p, int map_key, const double* lo,
                        long long lrows, long long lo_ld, const double* hi, long long hi_ld,
                        int width, const int* width_ptr, long long cap, double* out, long long ldo,
-                       double* part, int variant, cudaStream_t stream);
+                       double* part, int variant, cudaStream_t stream, double* side = nullptr,
+                       long long side_ld = 0, long long side_qstride = 0);
 
 // out[row][c] = sum over the reduced index of P[a + Da*b][c] * F[idx][c]
 // (reduce_b: rows a < rows_out, sum b < Db with F[b]; else rows b, sum a < La

@@ -460,7 +460,8 @@ int launch_mttkrp(Tensor& t, int mode, const FactorSet& f, int width, const int*
 int launch_contraction(Tensor& t, const ModePlan& p, int map_key, const double* lo,
                        long long lrows, long long lo_ld, const double* hi, long long hi_ld,
                        int width, const int* width_ptr, long long cap, double* out, long long ldo,
-                       double* part, int variant, cudaStream_t stream) {
+                       double* part, int variant, cudaStream_t stream, double* side,
+                       long long side_ld, long long side_qstride) {
   if (variant < 0) variant = choose_variant(p.M, cap, p.S);
   const VariantEntry& ve = kVariants[variant];
   const int sms = sm_count(t.device);
@@ -477,8 +478,10 @@ int launch_contraction(Tensor& t, const ModePlan& p, int map_key, const double* 
       rc = encode_map_3d(&m, t.data, p.D[0], p.D[1], p.D[2], BM + kPad, kBK, 1);
     else if (p.role == kRoleMiddle)
       rc = encode_map_3d(&m, t.data, p.D[0], p.D[1], p.D[2], kBK + kPad, BM, 1);
-    else
+    else if (p.role == kRoleLast)
       rc = encode_map_3d(&m, t.data, p.D[0], p.D[1], p.D[2], kBK + kPad, 1, BM);
+    else  // kRoleFirstQP: (m, q, p) -> smem [k][m]
+      rc = encode_map_3d(&m, t.data, p.D[0], p.D[1], p.D[2], BM + kPad, 1, kBK);
     if (rc) return rc;
     it = t.amaps.emplace(key, m).first;
   }
@@ -503,13 +506,17 @@ int launch_contraction(Tensor& t, const ModePlan& p, int map_key, const double* 
   a.out = p.S > 1 ? part : out;
   a.ldo = p.S > 1 ? lo_ld : ldo;
   a.part_stride = (long long)p.M * lo_ld;
+  a.side = side;
+  a.ld_side = side_ld;
+  a.side_qstride = side_qstride;
 
   const long long tm = (p.M + ve.info.BM - 1) / ve.info.BM;
   const long long tn = (cap + ve.info.BN - 1) / ve.info.BN;
   const long long units = tm * tn * p.S;
   const long long slots = (long long)ve.occupancy() * sms;
   dim3 grid((unsigned)std::max<long long>(1, std::min(units, slots)));
-  CALS_CUDA_TRY(ve.launch(grid, mapA, mapB, a, p.role != kRoleFirst, stream));
+  const bool kcontig = p.role == kRoleMiddle || p.role == kRoleLast;
+  CALS_CUDA_TRY(ve.launch(grid, mapA, mapB, a, kcontig, stream));
   if (p.S > 1) {
     const long long pairs = p.M * ((cap + 1) / 2);
     const int blocks = (int)std::max<long long>(1, std::min<long long>(sms * 8, (pairs + 255) / 256));
@@ -532,7 +539,7 @@ __global__ void partial_ttv_kernel(const double* __restrict__ P, long long ld, l
                                    const int* width_ptr, int width, long long rows_out,
                                    double* __restrict__ out, long long ldo) {
   const int W = width_ptr ? *width_ptr : width;
-  const long long n = rows_out * W;
+  const long long n = (reduce_b ? rows_out : (rows_out + 3) / 4) * W;
   for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < n;
        e += (long long)gridDim.x * blockDim.x) {
     const long long row = e / W;
@@ -548,6 +555,29 @@ __global__ void partial_ttv_kernel(const double* __restrict__ P, long long ld, l
       p = P + row * Da * ld + c;
       pstep = ld;
       L = La;
+    }
+    if (!reduce_b) {
+      // 4 output rows per thread share each F[a][c] load
+      const long long r4 = row * 4;
+      if (r4 >= rows_out) continue;
+      const int nr = (int)min(4LL, rows_out - r4);
+      const double* p4 = P + r4 * Da * ld + c;
+      const long long rs = Da * ld;
+      double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+      for (long long a = 0; a < L; ++a) {
+        const double fa = __ldg(f + a * ldf);
+        const double* pa = p4 + a * ld;
+        a0 = fma(__ldg(pa), fa, a0);
+        if (nr > 1) a1 = fma(__ldg(pa + rs), fa, a1);
+        if (nr > 2) a2 = fma(__ldg(pa + 2 * rs), fa, a2);
+        if (nr > 3) a3 = fma(__ldg(pa + 3 * rs), fa, a3);
+      }
+      double* o = out + r4 * ldo + c;
+      o[0] = a0;
+      if (nr > 1) o[ldo] = a1;
+      if (nr > 2) o[2 * ldo] = a2;
+      if (nr > 3) o[3 * ldo] = a3;
+      continue;
     }
     double acc = 0.0;
     long long i = 0;

@@ -32,7 +32,10 @@
 
 namespace cals {
 
-enum Role : int { kRoleFirst = 0, kRoleMiddle = 1, kRoleLast = 2 };
+// FIRST_QP: view (m, q, p) -- mode 0 with the slab index on dim 1 and the
+// contracted index on dim 2; its per-slab products are the dimension-tree
+// partial Y[i, j, :] = sum_k X[i,j,k] A2[k, :] (see `side` below).
+enum Role : int { kRoleFirst = 0, kRoleMiddle = 1, kRoleLast = 2, kRoleFirstQP = 3 };
 
 constexpr int kBK = 16;   // p-tile (DMMA k extent per pipeline stage)
 constexpr int kPad = 4;   // extra inner-dimension elements per smem row: pitch = 4 mod 16
@@ -51,6 +54,11 @@ struct MttkrpArgs {
   double* out;         // S == 1: [M][ldo]; S > 1: partials [S][M][ldo]
   long long ldo;
   long long part_stride;
+  // optional side output of every per-slab product (before the Hi scaling):
+  // side[(m + side_qstride * q) * ld_side + c]  -- the dimension-tree partial
+  double* side;
+  long long ld_side;
+  long long side_qstride;
 };
 
 template <int MI, int NI, int WM, int WN>
@@ -147,8 +155,10 @@ __global__ void __launch_bounds__(TileCfg<MI, NI, WM, WN>::kThreads, 2)
               tma_load_3d(sa, &tmA, &full[stage], m0, p0, q);
             else if (args.role == kRoleMiddle)
               tma_load_3d(sa, &tmA, &full[stage], p0, m0, q);
-            else
+            else if (args.role == kRoleLast)
               tma_load_3d(sa, &tmA, &full[stage], p0, q, m0);
+            else
+              tma_load_3d(sa, &tmA, &full[stage], m0, q, p0);
             tma_load_2d(sb, &tmB, &full[stage], c0, p0);
             if (++stage == STAGES) { stage = 0; phase ^= 1u; }
           }
@@ -221,6 +231,23 @@ __global__ void __launch_bounds__(TileCfg<MI, NI, WM, WN>::kThreads, 2)
         __syncwarp();
         if (lane == 0) mbar_arrive(&empty[stage]);
         if (++stage == STAGES) { stage = 0; phase ^= 1u; }
+      }
+      if (args.side) {
+        // dimension-tree partial: the unscaled slab product, written once
+#pragma unroll
+        for (int i = 0; i < MI; ++i) {
+          const int m = m0 + wm * 8 * MI + 8 * i + r;
+          if (m >= args.M) continue;
+          double* srow = args.side + ((long long)m + args.side_qstride * q) * args.ld_side;
+#pragma unroll
+          for (int j = 0; j < NI; ++j) {
+            const int c = cw + 8 * j;
+            if (c + 1 < W)
+              __stcg(reinterpret_cast<double2*>(srow + c), make_double2(t[i][j][0], t[i][j][1]));
+            else if (c < W)
+              __stcg(srow + c, t[i][j][0]);
+          }
+        }
       }
       // Khatri-Rao factor of the q-slab: one DFMA per accumulator element.
 #pragma unroll
