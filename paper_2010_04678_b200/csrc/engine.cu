@@ -109,7 +109,7 @@ __global__ void __launch_bounds__(kUpdThreads) engine_update_kernel(EngState* st
       // Gramians of the admitted starting point (driver.py:203-205)
       for (int i = 1; i < N; ++i) {
         if constexpr (RB > 0)
-          block_gram_fast<RB>(st->F[i] + off, ld, (int)st->dims[i], R, X, gram(i));
+          block_gram_fast(st->F[i] + off, ld, (int)st->dims[i], R, X, gram(i));
         else
           block_gram(st->F[i], ld, off, (int)st->dims[i], R, gram(i));
       }
@@ -146,10 +146,10 @@ __global__ void __launch_bounds__(kUpdThreads) engine_update_kernel(EngState* st
       } else {
         bool done = false;
         if constexpr (RB > 0) {
-          __shared__ double inv_diag[RB > 0 ? RB : 1];
-          if (warp_cholesky_reg<RB>(H, R, inv_diag, &flag)) {
-            done = block_solve_gram_fast<RB>(H, inv_diag, R, Mb, ld, rows, st->F[n] + off, ld, X,
-                                             gram(n), n == N - 1, &inner, red);
+          __shared__ double inv_diag[kFastR];
+          if (warp_cholesky_fast(H, R, inv_diag, &flag)) {
+            done = block_solve_gram_fast(H, inv_diag, R, Mb, ld, rows, st->F[n] + off, ld, X,
+                                         gram(n), n == N - 1, &inner, red);
             have_inner = done && n == N - 1;
           }
         }
@@ -217,9 +217,7 @@ __global__ void __launch_bounds__(kUpdThreads) engine_update_kernel(EngState* st
 
 using UpdateKernel = void (*)(EngState*, int, int);
 static UpdateKernel update_kernel_for(int max_rank, int* rb) {
-  if (max_rank <= 8) { *rb = 8; return engine_update_kernel<8>; }
-  if (max_rank <= 16) { *rb = 16; return engine_update_kernel<16>; }
-  if (max_rank <= 32) { *rb = 32; return engine_update_kernel<32>; }
+  if (max_rank <= kFastR) { *rb = kFastR; return engine_update_kernel<kFastR>; }
   *rb = 0;
   return engine_update_kernel<0>;
 }

@@ -562,15 +562,37 @@ __global__ void partial_ttv_kernel(const double* __restrict__ P, long long ld, l
       if (r4 >= rows_out) continue;
       const int nr = (int)min(4LL, rows_out - r4);
       const double* p4 = P + r4 * Da * ld + c;
-      const long long rs = Da * ld;
+      // rows past the end alias the last valid row (loaded, never stored)
+      const long long rs1 = (nr > 1 ? 1 : 0) * Da * ld, rs2 = (nr > 2 ? 2 : nr - 1) * Da * ld,
+                      rs3 = (nr > 3 ? 3 : nr - 1) * Da * ld;
       double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
-      for (long long a = 0; a < L; ++a) {
+      long long a = 0;
+      for (; a + 4 <= L; a += 4) {
+        double fv[4], pv[4][4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          fv[u] = __ldg(f + (a + u) * ldf);
+          const double* pa = p4 + (a + u) * ld;
+          pv[u][0] = __ldg(pa);
+          pv[u][1] = __ldg(pa + rs1);
+          pv[u][2] = __ldg(pa + rs2);
+          pv[u][3] = __ldg(pa + rs3);
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          a0 = fma(pv[u][0], fv[u], a0);
+          a1 = fma(pv[u][1], fv[u], a1);
+          a2 = fma(pv[u][2], fv[u], a2);
+          a3 = fma(pv[u][3], fv[u], a3);
+        }
+      }
+      for (; a < L; ++a) {
         const double fa = __ldg(f + a * ldf);
         const double* pa = p4 + a * ld;
         a0 = fma(__ldg(pa), fa, a0);
-        if (nr > 1) a1 = fma(__ldg(pa + rs), fa, a1);
-        if (nr > 2) a2 = fma(__ldg(pa + 2 * rs), fa, a2);
-        if (nr > 3) a3 = fma(__ldg(pa + 3 * rs), fa, a3);
+        a1 = fma(__ldg(pa + rs1), fa, a1);
+        a2 = fma(__ldg(pa + rs2), fa, a2);
+        a3 = fma(__ldg(pa + rs3), fa, a3);
       }
       double* o = out + r4 * ldo + c;
       o[0] = a0;

@@ -229,22 +229,26 @@ __device__ inline bool block_update(double* H, double* Hsave, double* V, double*
 }
 
 // ---------------------------------------------------------------------------
-// Fast path for R <= RB (RB in {8, 16, 32}): one thread per factor row keeps
-// the row in registers; triangular solves in dpotrs/dtrsm order (forward:
-// for each a, subtract k ascending then divide; back: k descending), and the
-// Gram refresh accumulated from a shared-memory chunk of solved rows (pair
-// sums over rows in ascending order -> deterministic).
+// Fast path for R <= 32 (every config rank): compact loops only -- the
+// update runs once per model per mode, so straight-line unrolled code would
+// be bound by instruction fetch.  One thread per factor row solves in place
+// in a shared-memory chunk Xs (row pitch P odd -> conflict-free), in
+// dpotrs/dtrsm order (forward: for each a subtract k ascending; back: k
+// descending) multiplying by the reciprocal diagonal as OpenBLAS's packed
+// trsm kernels do; the same chunk feeds the Gram refresh (pair sums over
+// rows in ascending order -> deterministic).
 
-template <int RB>
+constexpr int kFastR = 32;
+constexpr int kFastNP = (kFastR * (kFastR + 1) / 2 + kUpdThreads - 1) / kUpdThreads;
+
+__device__ __forceinline__ int fast_pitch(int R) { return (R & 1) ? R : R + 1; }
+
 struct FastPairs {
-  static constexpr int P = RB + 1;  // odd pitch: conflict-free row writes
-  static constexpr int NP = (RB * (RB + 1) / 2 + kUpdThreads - 1) / kUpdThreads;
-  int a[NP], b[NP];
-  double acc[NP];
+  int a[kFastNP], b[kFastNP];
+  double acc[kFastNP];
   __device__ void init(int R) {
     const int npairs = R * (R + 1) / 2;
-#pragma unroll
-    for (int j = 0; j < NP; ++j) {
+    for (int j = 0; j < kFastNP; ++j) {
       const int p = threadIdx.x + j * kUpdThreads;
       acc[j] = 0.0;
       a[j] = -1;
@@ -260,21 +264,28 @@ struct FastPairs {
       }
     }
   }
-  // rows [0, cnt) of the chunk Xs[row * P + col]
-  __device__ void accumulate(const double* Xs, int cnt) {
-#pragma unroll
-    for (int j = 0; j < NP; ++j) {
+  __device__ void accumulate(const double* Xs, int P, int cnt) {
+    for (int j = 0; j < kFastNP; ++j) {
       if (a[j] < 0) continue;
-      double s = acc[j];
       const double* pa = Xs + a[j];
       const double* pb = Xs + b[j];
-      for (int r = 0; r < cnt; ++r) s = fma(pa[r * P], pb[r * P], s);
+      double s = acc[j];
+      int r = 0;
+      for (; r + 4 <= cnt; r += 4) {
+        const double x0 = pa[r * P], y0 = pb[r * P], x1 = pa[(r + 1) * P], y1 = pb[(r + 1) * P];
+        const double x2 = pa[(r + 2) * P], y2 = pb[(r + 2) * P], x3 = pa[(r + 3) * P],
+                     y3 = pb[(r + 3) * P];
+        s = fma(x0, y0, s);
+        s = fma(x1, y1, s);
+        s = fma(x2, y2, s);
+        s = fma(x3, y3, s);
+      }
+      for (; r < cnt; ++r) s = fma(pa[r * P], pb[r * P], s);
       acc[j] = s;
     }
   }
   __device__ void store(double* G, int R) const {
-#pragma unroll
-    for (int j = 0; j < NP; ++j) {
+    for (int j = 0; j < kFastNP; ++j) {
       if (a[j] < 0) continue;
       G[a[j] * R + b[j]] = acc[j];
       G[b[j] * R + a[j]] = acc[j];
@@ -282,45 +293,31 @@ struct FastPairs {
   }
 };
 
-// Register-resident upper Cholesky by warp 0 for R <= RB <= 32: lane b holds
-// column b of H; step k broadcasts the pivot and row k with shuffles, so the
-// only serial chain is one sqrt + one divide per step.  Writes U into the
-// upper triangle of H and 1/U[k][k] into inv_diag (the row solves multiply by
-// the reciprocal, as OpenBLAS's packed trsm kernels do).  Fails like dpotrf.
-template <int RB>
-__device__ inline bool warp_cholesky_reg(double* H, int R, double* inv_diag, int* flag) {
+// Upper Cholesky of H (smem, R <= 32) by warp 0, lane b owning column b;
+// row k of U is broadcast with shuffles.  U overwrites the upper triangle;
+// inv_diag[k] = 1/U[k][k].  Fails like dpotrf (pivot <= 0 or NaN).
+__device__ inline bool warp_cholesky_fast(double* H, int R, double* inv_diag, int* flag) {
   if (threadIdx.x < 32) {
     const int lane = threadIdx.x;
-    double c[RB];
-#pragma unroll
-    for (int a = 0; a < RB; ++a) c[a] = (a < R && lane < R) ? H[a * R + lane] : 0.0;
     bool ok = true;
-#pragma unroll
-    for (int k = 0; k < RB; ++k) {
-      if (k < R && ok) {
-        const double piv = __shfl_sync(0xffffffffu, c[k], k);
-        if (!(piv > 0.0)) {
-          ok = false;
-        } else {
-          const double u = sqrt(piv);
-          if (lane == k) {
-            c[k] = u;
-            inv_diag[k] = 1.0 / u;
-          } else if (lane > k) {
-            c[k] = c[k] / u;
-          }
-#pragma unroll
-          for (int a = k + 1; a < RB; ++a) {
-            const double uka = __shfl_sync(0xffffffffu, c[k], a);
-            if (a < R && lane >= a) c[a] = fma(-uka, c[k], c[a]);
-          }
-        }
+    for (int k = 0; k < R; ++k) {
+      const double piv = H[k * R + k];
+      if (!(piv > 0.0)) {
+        ok = false;
+        break;
       }
-    }
-    if (ok && lane < R) {
-#pragma unroll
-      for (int a = 0; a < RB; ++a)
-        if (a <= lane) H[a * R + lane] = c[a];
+      const double u = sqrt(piv);
+      double ukb = 0.0;
+      if (lane == k) ukb = u;
+      else if (lane > k && lane < R) ukb = H[k * R + lane] / u;
+      __syncwarp();
+      if (lane >= k && lane < R) H[k * R + lane] = ukb;
+      if (lane == k) inv_diag[k] = 1.0 / u;
+      for (int a = k + 1; a < R; ++a) {
+        const double uka = __shfl_sync(0xffffffffu, ukb, a);
+        if (lane >= a && lane < R) H[a * R + lane] = fma(-uka, ukb, H[a * R + lane]);
+      }
+      __syncwarp();
     }
     if (lane == 0) *flag = ok ? 1 : 0;
   }
@@ -329,37 +326,33 @@ __device__ inline bool warp_cholesky_reg(double* H, int R, double* inv_diag, int
 }
 
 // Gram of an existing column block (rows x R at F + off), chunked through Xs.
-template <int RB>
 __device__ inline void block_gram_fast(const double* F, long long ld, int rows, int R, double* Xs,
                                        double* G) {
-  constexpr int P = FastPairs<RB>::P;
-  FastPairs<RB> pr;
+  const int P = fast_pitch(R);
+  FastPairs pr;
   pr.init(R);
   for (int base = 0; base < rows; base += kUpdThreads) {
     const int i = base + threadIdx.x;
     if (i < rows) {
       const double* row = F + (long long)i * ld;
-#pragma unroll
-      for (int a = 0; a < RB; ++a)
-        if (a < R) Xs[threadIdx.x * P + a] = row[a];
+      for (int a = 0; a < R; ++a) Xs[threadIdx.x * P + a] = row[a];
     }
     __syncthreads();
-    pr.accumulate(Xs, min(kUpdThreads, rows - base));
+    pr.accumulate(Xs, P, min(kUpdThreads, rows - base));
     __syncthreads();
   }
   pr.store(G, R);
 }
 
-// Solve every row of the block against the upper Cholesky factor U (smem),
-// write A, refresh G = A^T A, and (want_inner) return sum(A o M).
-// Returns false when a solution entry is non-finite (caller -> pinv path).
-template <int RB>
-__device__ inline bool block_solve_gram_fast(const double* U, const double* inv_diag, int R, const double* Mb, long long ldm,
-                                             int rows, double* A, long long lda, double* Xs,
-                                             double* G, bool want_inner, double* inner,
-                                             double* red) {
-  constexpr int P = FastPairs<RB>::P;
-  FastPairs<RB> pr;
+// Solve every row of the block against U (smem) / inv_diag, write A,
+// refresh G = A^T A and (want_inner) return sum(A o M).  Returns false when
+// a solution entry is non-finite (caller -> pinv path).
+__device__ inline bool block_solve_gram_fast(const double* U, const double* inv_diag, int R,
+                                             const double* Mb, long long ldm, int rows, double* A,
+                                             long long lda, double* Xs, double* G,
+                                             bool want_inner, double* inner, double* red) {
+  const int P = fast_pitch(R);
+  FastPairs pr;
   pr.init(R);
   double dot = 0.0;
   int bad = 0;
@@ -367,39 +360,31 @@ __device__ inline bool block_solve_gram_fast(const double* U, const double* inv_
     const int i = base + threadIdx.x;
     if (i < rows) {
       const double* m = Mb + (long long)i * ldm;
-      double x[RB];
-#pragma unroll
-      for (int a = 0; a < RB; ++a) x[a] = a < R ? m[a] : 0.0;
-#pragma unroll
-      for (int k = 0; k < RB; ++k) {
-        if (k < R) {
-          x[k] = x[k] * inv_diag[k];
-#pragma unroll
-          for (int a = k + 1; a < RB; ++a)
-            if (a < R) x[a] = fma(-U[k * R + a], x[k], x[a]);
-        }
+      double* x = Xs + threadIdx.x * P;
+      for (int a = 0; a < R; ++a) x[a] = m[a];
+      for (int k = 0; k < R; ++k) {  // U^T y = m
+        const double xk = x[k] * inv_diag[k];
+        x[k] = xk;
+        const double* urow = U + k * R;
+#pragma unroll 4
+        for (int a = k + 1; a < R; ++a) x[a] = fma(-urow[a], xk, x[a]);
       }
-#pragma unroll
-      for (int k = RB - 1; k >= 0; --k) {
-        if (k < R) {
-          x[k] = x[k] * inv_diag[k];
-#pragma unroll
-          for (int a = 0; a < k; ++a) x[a] = fma(-U[a * R + k], x[k], x[a]);
-        }
+      for (int k = R - 1; k >= 0; --k) {  // U x = y
+        const double xk = x[k] * inv_diag[k];
+        x[k] = xk;
+#pragma unroll 4
+        for (int a = 0; a < k; ++a) x[a] = fma(-U[a * R + k], xk, x[a]);
       }
       double* o = A + (long long)i * lda;
-#pragma unroll
-      for (int a = 0; a < RB; ++a) {
-        if (a < R) {
-          bad |= !isfinite(x[a]);
-          o[a] = x[a];
-          Xs[threadIdx.x * P + a] = x[a];
-          if (want_inner) dot = fma(x[a], m[a], dot);
-        }
+      for (int a = 0; a < R; ++a) {
+        const double v = x[a];
+        bad |= !isfinite(v);
+        o[a] = v;
+        if (want_inner) dot = fma(v, m[a], dot);
       }
     }
     __syncthreads();
-    pr.accumulate(Xs, min(kUpdThreads, rows - base));
+    pr.accumulate(Xs, P, min(kUpdThreads, rows - base));
     __syncthreads();
   }
   if (__syncthreads_or(bad)) return false;
