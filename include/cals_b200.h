@@ -105,6 +105,24 @@ int cals_engine_trace(cals_engine* e, int32_t* widths, int32_t* n_active, double
                       int capacity, int* count);
 int cals_engine_variant(cals_engine* e, int mode, int* variant, int* bm, int* bn, int* splits);
 
+/* Step-wise driving of the same loop (what cals_engine_run replays as a CUDA
+ * graph), for host-orchestrated runs that interleave collectives: the
+ * mode-0-sharded configuration all-reduces the partial MTTKRP of modes >= 1
+ * (between _mttkrp and _update) and the mode-0 Gramians (after _update(0)).
+ * One driver iteration = for n: enqueue_mttkrp(n), enqueue_update(n); then
+ * enqueue_plan.  cals_engine_done reads the mapped flag the plan kernel sets.
+ * cals_engine_buffers exposes the device MTTKRP output ([max I][ld]), the
+ * Gramians ([order][gram_stride], per-model R_k x R_k blocks) and the factor
+ * buffers ([I_n][ld] each). */
+int cals_engine_begin(cals_engine* e, double tol, int max_iterations, double sqnorm,
+                      void* stream);
+int cals_engine_enqueue_mttkrp(cals_engine* e, int mode, void* stream);
+int cals_engine_enqueue_update(cals_engine* e, int mode, void* stream);
+int cals_engine_enqueue_plan(cals_engine* e, void* stream);
+int cals_engine_done(cals_engine* e, int* done);
+int cals_engine_buffers(cals_engine* e, double** mttkrp_out, double** grams, int64_t* ld,
+                        int64_t* gram_stride, double** factors);
+
 /* ---- diagnostics (no reference counterpart) ------------------------------
  * Live FP64 tensor-core peak (DMMA.8x8x4 on every SM, TFLOP/s): the
  * roofline denominator for the fused MTTKRP. */

@@ -135,9 +135,31 @@ __global__ void __launch_bounds__(kUpdThreads) engine_update_kernel(EngState* st
         bad |= !isfinite(h);
       }
       const double* Mb = st->Mout + off;
-      for (int i = threadIdx.x; i < rows; i += blockDim.x) {
-        const double* mrow = Mb + (long long)i * ld;
-        for (int a = 0; a < R; ++a) bad |= !isfinite(mrow[a]);
+      __shared__ double inv_diag[kFastR];
+      bool chol_ok = false;
+      if constexpr (RB > 0) {
+        // warp 0 factors H while the other warps check the whole M block and
+        // stage its first chunk of rows into X (the reference checks before
+        // touching anything, als.py:84-85; a NaN pivot is caught below too)
+        __syncthreads();
+        if (threadIdx.x < 32) {
+          warp_cholesky_fast_nosync(H, R, inv_diag, &flag);
+        } else {
+          const int P = fast_pitch(R);
+          for (int i = threadIdx.x - 32; i < rows; i += blockDim.x - 32) {
+            const double* mrow = Mb + (long long)i * ld;
+            for (int a = 0; a < R; ++a) {
+              const double v = mrow[a];
+              bad |= !isfinite(v);
+              if (i < kUpdThreads) X[i * P + a] = v;
+            }
+          }
+        }
+      } else {
+        for (int i = threadIdx.x; i < rows; i += blockDim.x) {
+          const double* mrow = Mb + (long long)i * ld;
+          for (int a = 0; a < R; ++a) bad |= !isfinite(mrow[a]);
+        }
       }
       if (__syncthreads_or(bad)) {
         // non-finite input: the reference raises ValueError -> FAILED (als.py:84-85)
@@ -146,10 +168,10 @@ __global__ void __launch_bounds__(kUpdThreads) engine_update_kernel(EngState* st
       } else {
         bool done = false;
         if constexpr (RB > 0) {
-          __shared__ double inv_diag[kFastR];
-          if (warp_cholesky_fast(H, R, inv_diag, &flag)) {
+          chol_ok = flag != 0;
+          if (chol_ok) {
             done = block_solve_gram_fast(H, inv_diag, R, Mb, ld, rows, st->F[n] + off, ld, X,
-                                         gram(n), n == N - 1, &inner, red);
+                                         gram(n), n == N - 1, &inner, red, true);
             have_inner = done && n == N - 1;
           }
         }
@@ -694,18 +716,19 @@ static int engine_reset(Engine* e, double tol, int max_iterations, double sqnorm
   return kOk;
 }
 
-static int enqueue_iteration(Engine* e, cudaStream_t stream) {
+// M_n -> Mout for the current layout (dimension-tree aware).
+static int enqueue_mode_mttkrp(Engine* e, int n, cudaStream_t stream) {
   Tensor& t = *e->t;
   const int N = e->order;
   FactorSet fs{};
-  for (int n = 0; n < N; ++n) fs.ptr[n] = e->h_st.F[n];
+  for (int i = 0; i < N; ++i) fs.ptr[i] = e->h_st.F[i];
   fs.ld = e->ld;
   const int* wptr = &e->d_st->width;
   const int sms = sm_count(t.device);
   double* const* F = e->h_st.F;
   double* Mo = e->h_st.Mout;
   const long long ld = e->ld, cap = e->capacity;
-  for (int n = 0; n < N; ++n) {
+  {
     int rc = kOk;
     if (e->tree == kTreeY && n == 0) {
       // M0 = sum_j A1[j] (sum_k X[:,j,k] A2[k]); the inner slab products are
@@ -729,14 +752,31 @@ static int enqueue_iteration(Engine* e, cudaStream_t stream) {
                          stream);
     }
     if (rc) return rc;
-    e->upd_kernel<<<e->upd_grid, kUpdThreads, e->upd_smem, stream>>>(e->d_st, n, e->upd_nthr);
-    CALS_CUDA_TRY(cudaGetLastError());
   }
+  return kOk;
+}
+
+static int enqueue_mode_update(Engine* e, int n, cudaStream_t stream) {
+  e->upd_kernel<<<e->upd_grid, kUpdThreads, e->upd_smem, stream>>>(e->d_st, n, e->upd_nthr);
+  CALS_CUDA_TRY(cudaGetLastError());
+  return kOk;
+}
+
+static int enqueue_plan(Engine* e, cudaStream_t stream) {
   engine_plan_kernel<<<1, 32, 0, stream>>>(e->d_st);
   CALS_CUDA_TRY(cudaGetLastError());
   engine_move_kernel<<<e->move_grid, 256, e->move_smem, stream>>>(e->d_st);
   CALS_CUDA_TRY(cudaGetLastError());
   return kOk;
+}
+
+static int enqueue_iteration(Engine* e, cudaStream_t stream) {
+  for (int n = 0; n < e->order; ++n) {
+    int rc = enqueue_mode_mttkrp(e, n, stream);
+    if (!rc) rc = enqueue_mode_update(e, n, stream);
+    if (rc) return rc;
+  }
+  return enqueue_plan(e, stream);
 }
 
 static int engine_capture(Engine* e, cudaStream_t stream) {
@@ -1008,6 +1048,58 @@ int cals_engine_trace(cals_engine* e, int32_t* widths, int32_t* n_active, double
     if (n_active) n_active[i] = a[i];
     if (seconds) seconds[i] = (double)(tt[i + 1] - tt[i]) * 1e-9;
   }
+  return kOk;
+}
+
+// ---- step-wise driving (host-orchestrated loops, e.g. the mode-0-sharded
+// configuration with an all-reduce between the MTTKRP and the update) ------
+int cals_engine_begin(cals_engine* e, double tol, int max_iterations, double sqnorm,
+                      void* stream) {
+  CALS_CHECK(e, kErrInvalid, "null engine");
+  CALS_CHECK(max_iterations >= 1, kErrInvalid, "max_iterations must be >= 1");
+  CALS_CHECK(sqnorm > 0.0, kErrInvalid, "tensor squared norm must be positive");
+  Engine* g = e->e;
+  cudaStream_t s = (cudaStream_t)stream;
+  int rc = engine_reset(g, tol, max_iterations, sqnorm, s);
+  if (rc) return rc;
+  if (g->n_models == 0) {
+    *g->h_done = 1;
+    return kOk;
+  }
+  return enqueue_plan(g, s);  // initial admission
+}
+
+int cals_engine_enqueue_mttkrp(cals_engine* e, int mode, void* stream) {
+  CALS_CHECK(e && mode >= 0 && mode < e->e->order, kErrInvalid, "bad argument");
+  return enqueue_mode_mttkrp(e->e, mode, (cudaStream_t)stream);
+}
+
+int cals_engine_enqueue_update(cals_engine* e, int mode, void* stream) {
+  CALS_CHECK(e && mode >= 0 && mode < e->e->order, kErrInvalid, "bad argument");
+  return enqueue_mode_update(e->e, mode, (cudaStream_t)stream);
+}
+
+int cals_engine_enqueue_plan(cals_engine* e, void* stream) {
+  CALS_CHECK(e, kErrInvalid, "null engine");
+  return enqueue_plan(e->e, (cudaStream_t)stream);
+}
+
+int cals_engine_done(cals_engine* e, int* done) {
+  CALS_CHECK(e && done, kErrInvalid, "null argument");
+  *done = *(volatile int*)e->e->h_done;
+  return kOk;
+}
+
+int cals_engine_buffers(cals_engine* e, double** mttkrp_out, double** grams, int64_t* ld,
+                        int64_t* gram_stride, double** factors) {
+  CALS_CHECK(e, kErrInvalid, "null engine");
+  Engine* g = e->e;
+  if (mttkrp_out) *mttkrp_out = g->h_st.Mout;
+  if (grams) *grams = g->h_st.grams;
+  if (ld) *ld = g->ld;
+  if (gram_stride) *gram_stride = g->gram_stride;
+  if (factors)
+    for (int n = 0; n < g->order; ++n) factors[n] = g->h_st.F[n];
   return kOk;
 }
 

@@ -18,7 +18,7 @@
 
 namespace cals {
 
-constexpr int kUpdThreads = 128;
+constexpr int kUpdThreads = 256;
 
 // deterministic block sum (fixed tree); `red` has >= blockDim.x doubles
 __device__ __forceinline__ double block_sum(double v, double* red) {
@@ -296,8 +296,8 @@ struct FastPairs {
 // Upper Cholesky of H (smem, R <= 32) by warp 0, lane b owning column b;
 // row k of U is broadcast with shuffles.  U overwrites the upper triangle;
 // inv_diag[k] = 1/U[k][k].  Fails like dpotrf (pivot <= 0 or NaN).
-__device__ inline bool warp_cholesky_fast(double* H, int R, double* inv_diag, int* flag) {
-  if (threadIdx.x < 32) {
+__device__ inline void warp_cholesky_fast_nosync(double* H, int R, double* inv_diag, int* flag) {
+  {
     const int lane = threadIdx.x;
     bool ok = true;
     for (int k = 0; k < R; ++k) {
@@ -321,6 +321,10 @@ __device__ inline bool warp_cholesky_fast(double* H, int R, double* inv_diag, in
     }
     if (lane == 0) *flag = ok ? 1 : 0;
   }
+}
+
+__device__ inline bool warp_cholesky_fast(double* H, int R, double* inv_diag, int* flag) {
+  if (threadIdx.x < 32) warp_cholesky_fast_nosync(H, R, inv_diag, flag);
   __syncthreads();
   return *flag != 0;
 }
@@ -350,7 +354,8 @@ __device__ inline void block_gram_fast(const double* F, long long ld, int rows, 
 __device__ inline bool block_solve_gram_fast(const double* U, const double* inv_diag, int R,
                                              const double* Mb, long long ldm, int rows, double* A,
                                              long long lda, double* Xs, double* G,
-                                             bool want_inner, double* inner, double* red) {
+                                             bool want_inner, double* inner, double* red,
+                                             bool first_chunk_staged = false) {
   const int P = fast_pitch(R);
   FastPairs pr;
   pr.init(R);
@@ -361,7 +366,8 @@ __device__ inline bool block_solve_gram_fast(const double* U, const double* inv_
     if (i < rows) {
       const double* m = Mb + (long long)i * ldm;
       double* x = Xs + threadIdx.x * P;
-      for (int a = 0; a < R; ++a) x[a] = m[a];
+      if (base > 0 || !first_chunk_staged)
+        for (int a = 0; a < R; ++a) x[a] = m[a];
       for (int k = 0; k < R; ++k) {  // U^T y = m
         const double xk = x[k] * inv_diag[k];
         x[k] = xk;

@@ -18,6 +18,15 @@ import numpy as np
 from . import _native
 
 
+class _CudaBuffer:
+    """Minimal ``__cuda_array_interface__`` exporter for engine-owned memory."""
+
+    def __init__(self, ptr: int, shape):
+        self.__cuda_array_interface__ = {"shape": tuple(int(s) for s in shape), "typestr": "<f8",
+                                         "data": (int(ptr), False), "version": 3,
+                                         "strides": None}
+
+
 @dataclass
 class EngineResults:
     pool: np.ndarray
@@ -127,6 +136,55 @@ class CalsEngine:
                      sec.ctypes.data, cap, C.byref(cnt))
         n = min(cnt.value, cap)
         return [(int(w[i]), int(a[i]), float(sec[i])) for i in range(n)]
+
+    # ------------------------------------------------------- step-wise
+    def begin(self, tol: float, max_iterations: int, sqnorm: float, stream=None):
+        import torch
+
+        s = stream if stream is not None else torch.cuda.current_stream().cuda_stream
+        _native.call("cals_engine_begin", self.handle, float(tol), int(max_iterations),
+                     float(sqnorm), s)
+
+    def enqueue_mttkrp(self, mode: int, stream=None):
+        import torch
+
+        s = stream if stream is not None else torch.cuda.current_stream().cuda_stream
+        _native.call("cals_engine_enqueue_mttkrp", self.handle, mode, s)
+
+    def enqueue_update(self, mode: int, stream=None):
+        import torch
+
+        s = stream if stream is not None else torch.cuda.current_stream().cuda_stream
+        _native.call("cals_engine_enqueue_update", self.handle, mode, s)
+
+    def enqueue_plan(self, stream=None):
+        import torch
+
+        s = stream if stream is not None else torch.cuda.current_stream().cuda_stream
+        _native.call("cals_engine_enqueue_plan", self.handle, s)
+
+    def done(self) -> bool:
+        d = C.c_int()
+        _native.call("cals_engine_done", self.handle, C.byref(d))
+        return bool(d.value)
+
+    def buffers(self) -> dict:
+        """Zero-copy torch views of the device buffers (``__cuda_array_interface__``)."""
+        import torch
+
+        mo, gr = C.c_void_p(), C.c_void_p()
+        ld, gs = C.c_int64(), C.c_int64()
+        fac = (C.c_void_p * self.order)()
+        _native.call("cals_engine_buffers", self.handle, C.byref(mo), C.byref(gr), C.byref(ld),
+                     C.byref(gs), fac)
+
+        def view(ptr, shape):
+            return torch.as_tensor(_CudaBuffer(ptr, shape), device="cuda")
+
+        return {"mttkrp": view(mo.value, (max(self.dims), ld.value)),
+                "grams": view(gr.value, (self.order, gs.value)),
+                "factors": [view(fac[n], (self.dims[n], ld.value)) for n in range(self.order)],
+                "ld": ld.value, "gram_stride": gs.value}
 
     def variant(self, mode: int) -> dict:
         v, bm, bn, s = C.c_int(), C.c_int(), C.c_int(), C.c_int()

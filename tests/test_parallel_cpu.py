@@ -1,0 +1,77 @@
+"""Multi-GPU host logic on CPU: snake partition and the world_size-2 gather
+path over the gloo backend (the GPU runner is replaced by a stub that fits
+nothing -- only the sharding / collective plumbing is under test here)."""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from paper_2010_04678_b200.parallel import run_sharded, shard_widths, snake_partition
+
+
+def test_snake_partition_balanced_and_complete():
+    ranks = [r for r in range(1, 21) for _ in range(25)]  # config 4: 500 models, W = 5250
+    for world in (1, 2, 4, 8):
+        parts = snake_partition(ranks, world)
+        assert sorted(i for p in parts for i in p) == list(range(len(ranks)))
+        w = shard_widths(ranks, world)
+        assert sum(w) == 5250
+        assert max(w) - min(w) <= 20  # within one model of the largest rank
+        for p in parts:
+            assert p == sorted(p)  # FIFO order kept inside a shard
+
+
+def test_snake_partition_edge_cases():
+    assert snake_partition([], 3) == [[], [], []]
+    assert snake_partition([5], 2) == [[0], []]
+    with pytest.raises(ValueError):
+        snake_partition([1], 0)
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    return port
+
+
+def _worker(rank, world, port, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_2010_04678_b200.model import Model, ModelStatus
+
+    models = [Model.random((4, 3, 2), r, np.random.default_rng(i), id=f"m{i}")
+              for i, r in enumerate([1, 2, 3, 4, 5, 6, 7])]
+
+    def stub_runner(t, ms, cfg, r_star):
+        assert sum(m.rank for m in ms) <= r_star
+        return [Model(id=m.id, rank=m.rank, factors=m.copy_factors(), iterations_done=rank,
+                      status=ModelStatus.ITERATION_CAP) for m in ms]
+
+    out = run_sharded(None, models, None, runner=stub_runner)
+    q.put((rank, [(m.id, m.iterations_done) for m in out]))
+    dist.destroy_process_group()
+
+
+def test_world_size_two_gloo_gather():
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = dict(q.get(timeout=120) for _ in procs)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    assert res[0] == res[1]  # every rank sees the full, identical result list
+    ids = [i for i, _ in res[0]]
+    assert sorted(ids) == sorted(f"m{i}" for i in range(7))
+    parts = snake_partition([1, 2, 3, 4, 5, 6, 7], 2)
+    assert ids == [f"m{i}" for i in parts[0]] + [f"m{i}" for i in parts[1]]
+    assert [it for _, it in res[0]] == [0] * len(parts[0]) + [1] * len(parts[1])
