@@ -101,7 +101,9 @@ __device__ __forceinline__ void unit_decode(int u, int tm, int tn, int& tile_m, 
 }
 
 template <int MI, int NI, int WM, int WN, bool KC>
-__global__ void __launch_bounds__(TileCfg<MI, NI, WM, WN>::kThreads, 2)
+// 2 CTAs x 5 warps per SM fit 200 registers per thread (per-warp allocation);
+// __launch_bounds__(.., 2) alone makes ptxas assume 6-warp granularity (168).
+__global__ void __maxnreg__(200)
     mttkrp_dmma_kernel(const __grid_constant__ CUtensorMap tmA,
                        const __grid_constant__ CUtensorMap tmB, const MttkrpArgs args) {
   using C = TileCfg<MI, NI, WM, WN>;
@@ -208,9 +210,7 @@ __global__ void __launch_bounds__(TileCfg<MI, NI, WM, WN>::kThreads, 2)
         const double* sb = sa + C::A_ELEMS;
         int p0, ks_lo, ks_hi;
         ptile(pt, args.Dp, p0, ks_lo, ks_hi);
-#pragma unroll
-        for (int ks = 0; ks < kBK / 4; ++ks) {
-          if (ks < ks_lo || ks >= ks_hi) continue;
+        auto kstep = [&](int ks) {
           const int k = 4 * ks + kq;
           double a[MI], b[NI];
           if constexpr (KC) {
@@ -227,6 +227,15 @@ __global__ void __launch_bounds__(TileCfg<MI, NI, WM, WN>::kThreads, 2)
           for (int i = 0; i < MI; ++i)
 #pragma unroll
             for (int j = 0; j < NI; ++j) dmma_8x8x4(t[i][j][0], t[i][j][1], a[i], b[j]);
+        };
+        if (ks_lo == 0 && ks_hi == kBK / 4) {
+          // full tile: branch-free, so fragment loads of step ks+1 overlap the
+          // DMMAs of step ks
+#pragma unroll
+          for (int ks = 0; ks < kBK / 4; ++ks) kstep(ks);
+        } else {
+#pragma unroll 1
+          for (int ks = ks_lo; ks < ks_hi; ++ks) kstep(ks);
         }
         __syncwarp();
         if (lane == 0) mbar_arrive(&empty[stage]);
