@@ -105,6 +105,14 @@ int cals_engine_trace(cals_engine* e, int32_t* widths, int32_t* n_active, double
                       int capacity, int* count);
 int cals_engine_variant(cals_engine* e, int mode, int* variant, int* bm, int* bn, int* splits);
 
+/* Line search (replaces als.py:127-144 extrapolate_factors as called from
+ * driver.py:250-259, 272-273): after every iteration each model holding a
+ * snapshot of its previous iterate is extrapolated to prev + alpha (curr -
+ * prev) (alpha <= 0 selects alpha = iteration^(1/3), als.py:56-59); ONE fused
+ * last-mode MTTKRP evaluates every candidate; a candidate with a lower error
+ * replaces the iterate.  Takes effect at the next cals_engine_run. */
+int cals_engine_set_line_search(cals_engine* e, int enabled, double alpha);
+
 /* Step-wise driving of the same loop (what cals_engine_run replays as a CUDA
  * graph), for host-orchestrated runs that interleave collectives: the
  * mode-0-sharded configuration all-reduces the partial MTTKRP of modes >= 1

@@ -209,11 +209,21 @@ class _Inst:
     error: float = np.inf
     fit: float = -np.inf
     grams: list = field(default_factory=list)
+    snapshot: list | None = None
     failed: bool = False
 
 
+def extrapolate(arr_flat, dims, sq, prev, curr, alpha):
+    """Candidate prev + alpha (curr - prev), its Gramians and exact error
+    (als.py:127-144)."""
+    cand = [np.asfortranarray(p + alpha * (c - p)) for p, c in zip(prev, curr)]
+    grams = [gramian(f) for f in cand]
+    m_last = mttkrp(arr_flat, dims, cand, len(dims) - 1)
+    return cand, grams, fast_error(sq, cand[-1], m_last, grams)
+
+
 def run_cals(arr_flat, dims, models, tol: float, max_iterations: int, r_star: int,
-             trace: list | None = None):
+             trace: list | None = None, ls: bool = False, ls_alpha: float | None = None):
     """Algorithm 4 of the paper as the reference driver executes it.
 
     ``models`` is ``[(id, rank, factors)]``.  Semantics restated from
@@ -274,6 +284,16 @@ def run_cals(arr_flat, dims, models, tol: float, max_iterations: int, r_star: in
                 continue
             sl = slice(inst.off, inst.off + inst.rank)
             e = fast_error(sq, bufs[-1][:, sl], m_fused[:, sl], inst.grams)
+            if ls and inst.snapshot is not None and np.isfinite(e):
+                # driver.py:250-259
+                alpha = ls_alpha if ls_alpha is not None else float(inst.iteration) ** (1.0 / 3.0)
+                cand, cgrams, ec = extrapolate(arr_flat, dims, sq, inst.snapshot,
+                                               [b[:, sl] for b in bufs], alpha)
+                if ec < e:
+                    for b, c in zip(bufs, cand):
+                        b[:, sl] = c
+                    inst.grams = cgrams
+                    e = ec
             if not np.isfinite(e):
                 inst.error, inst.fit = float(e), -np.inf
                 retiring.append((inst, FAILED))
@@ -286,6 +306,8 @@ def run_cals(arr_flat, dims, models, tol: float, max_iterations: int, r_star: in
                 retiring.append((inst, ITERATION_CAP))
             else:
                 inst.f_prev = fit
+                if ls:  # driver.py:272-273
+                    inst.snapshot = [np.array(b[:, sl], order="F") for b in bufs]
         n_active = len(reg)
         for inst, status in retiring:
             sl = slice(inst.off, inst.off + inst.rank)

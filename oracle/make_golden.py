@@ -156,6 +156,33 @@ def main() -> None:
     run_case("order2", o2, build_models(o2.dims, [1, 2, 3], per_rank=2, seed=4), 0.0, 6, 12)
     o4 = generate_synthetic((5, 4, 6, 3), 2, 0.05, seed=5)
     run_case("order4", o4, build_models(o4.dims, [1, 2, 3], per_rank=2, seed=6), 0.0, 6, 12)
+    # line search in the fused driver (driver.py:250-259, 272-273)
+    from cals.als import LineSearchConfig
+
+    def run_ls_case(name, tensor, models, tol, iters, r_star, alpha):
+        trace: list = []
+        out = run(tensor, models, ConvergenceConfig(tol=tol, max_iterations=iters),
+                  mode=ExecutionMode.CALS, r_star=r_star, trace=trace,
+                  ls=LineSearchConfig(enabled=True, alpha=alpha))
+        d = {"order": np.array([m.id for m in out]),
+             "status": np.array([m.status.value for m in out]),
+             "iterations": np.array([m.iterations_done for m in out]),
+             "fit": np.array([m.fit for m in out]), "error": np.array([m.error for m in out]),
+             "widths": np.array([s.meta["width"] for s in trace]),
+             "n_active": np.array([s.meta["n_active"] for s in trace])}
+        for m in out:
+            for n, f in enumerate(m.factors):
+                d[f"{m.id}_f{n}"] = f
+        np.savez(os.path.join(OUT, f"run_{name}.npz"), **d)
+        meta["cases"][name] = {"dims": list(tensor.dims), "tol": tol, "max_iterations": iters,
+                               "r_star": r_star, "ls_alpha": alpha}
+
+    run_ls_case("ls_cube_root", small, build_models(small.dims, [1, 2, 3, 4], 2, seed=1),
+                0.0, 8, 20, None)
+    run_ls_case("ls_const", small, build_models(small.dims, [2, 3], 2, seed=7), 0.0, 8, 6, 1.5)
+    run_ls_case("ls_c1_tol", c1, build_models(c1.dims, [1, 2, 3, 4, 5], 4, seed=1),
+                1e-6, 1000, 60, None)
+
     # failure isolation (test_driver.py:117-135)
     rng = np.random.default_rng(66)
     fd = (4, 4, 3)

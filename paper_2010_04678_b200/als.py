@@ -108,16 +108,45 @@ def fit_from_error(e: float, t_sqnorm: float) -> float:
     return 1.0 - math.sqrt(e) / math.sqrt(t_sqnorm)
 
 
-_NEXT = ("line search and non-negative updates are the next rows of the hot-path "
-         "scope (SURVEY.md section 8f) and are not implemented on the GPU yet")
+_NEXT = ("non-negative (NNLS) updates are the next row of the hot-path scope "
+         "(SURVEY.md section 8f) and are not implemented on the GPU yet")
 
 
-def extrapolate_factors(*args, **kwargs):
-    raise NotImplementedError(_NEXT)
+def extrapolate_factors(t, prev, curr, alpha: float, ws=None, variant_table=None):
+    """Candidate ``prev + alpha * (curr - prev)``, its Gramians and exact
+    error from a fresh last-mode MTTKRP on the GPU (als.py:127-144).  Inside
+    ``run(..., ls=...)`` the engine evaluates every model's candidate with
+    one fused MTTKRP instead."""
+    from .mttkrp import mttkrp, select_variant
+    from .tensor import gramian
+
+    cand = [np.asfortranarray(p + alpha * (c - p)) for p, c in zip(prev, curr)]
+    grams = [gramian(f) for f in cand]
+    n_last = t.order - 1
+    variant = select_variant(t.dims, n_last, cand[0].shape[1], variant_table)
+    m_last = mttkrp(t, cand, n_last, variant=variant, ws=ws)
+    return cand, grams, fast_error(t.sqnorm, cand, m_last, grams)
 
 
-def line_search_step(*args, **kwargs):
-    raise NotImplementedError(_NEXT)
+def line_search_step(prev, curr, cfg: LineSearchConfig, t, iteration: int | None = None,
+                     ws=None):
+    """Extrapolate from two consecutive iterates and keep whichever errs less
+    (als.py:147-182)."""
+    from .model import Model
+
+    if not cfg.enabled:
+        raise ValueError("line search disabled in config")
+    if prev.rank != curr.rank or prev.dims != curr.dims:
+        raise ValueError("prev/curr models do not conform")
+    if iteration is None:
+        iteration = max(curr.iterations_done, 2)
+    cand, _, e_cand = extrapolate_factors(t, prev.factors, curr.factors,
+                                          alpha_for_iteration(cfg, iteration), ws)
+    if not (e_cand < curr.error):
+        return curr
+    return Model(id=curr.id, rank=curr.rank, factors=cand, error=e_cand,
+                 fit=fit_from_error(e_cand, t.sqnorm), iterations_done=curr.iterations_done,
+                 status=curr.status, meta=dict(curr.meta))
 
 
 def nnls_solve_row(*args, **kwargs):

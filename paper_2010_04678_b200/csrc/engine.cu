@@ -76,7 +76,44 @@ struct EngState {
   int* tr_active;
   unsigned long long* tr_time;
   volatile int* host_done;
+  // line search (als.py:127-144, driver.py:250-259,272-273): snapshots S of
+  // the previous iterate, candidates C, their Gramians, per-model flags
+  int ls_enabled;
+  double ls_alpha;  // <= 0: alpha = iteration^(1/3)
+  double* S[kMaxOrder];
+  double* Cb[kMaxOrder];
+  double* cgrams;
+  int* has_snap;
+  int* ls_act;
+  double* e_tmp;
 };
+
+// Stopping rule for model k with squared error e (driver.py:260-273); the
+// caller has already incremented iters[k].  Thread 0 only.
+__device__ inline void decide_model(EngState* st, int k, double e) {
+  const int it = st->iters[k];
+  if (st->failed[k]) {
+    st->err[k] = nan("");
+    st->fit[k] = -INFINITY;
+    st->status[k] = kFailed;
+    return;
+  }
+  if (!isfinite(e)) {
+    st->err[k] = e;
+    st->fit[k] = -INFINITY;
+    st->status[k] = kFailed;
+    return;
+  }
+  const double f = 1.0 - sqrt(e) / sqrt(st->sqnorm);
+  st->err[k] = e;
+  st->fit[k] = f;
+  if (st->tol > 0.0 && f - st->f_prev[k] < st->tol)
+    st->status[k] = kConverged;
+  else if (it >= st->max_iterations)
+    st->status[k] = kCap;
+  else
+    st->f_prev[k] = f;
+}
 
 // ------------------------------------------------------------------ update --
 // RB > 0: fast path (every rank <= RB, rows in registers, chunked Gram);
@@ -207,33 +244,123 @@ __global__ void __launch_bounds__(kUpdThreads) engine_update_kernel(EngState* st
         msq = block_sum(mpart, red);
       }
       if (threadIdx.x == 0) {
-        const int it = ++st->iters[k];
-        if (st->failed[k]) {
-          st->err[k] = nan("");
-          st->fit[k] = -INFINITY;
-          st->status[k] = kFailed;
-        } else {
-          double e = st->sqnorm + msq - 2.0 * inner;
-          e = e > 0.0 ? e : 0.0;
-          if (!isfinite(e)) {
-            st->err[k] = e;
-            st->fit[k] = -INFINITY;
-            st->status[k] = kFailed;
-          } else {
-            const double f = 1.0 - sqrt(e) / sqrt(st->sqnorm);
-            st->err[k] = e;
-            st->fit[k] = f;
-            if (st->tol > 0.0 && f - st->f_prev[k] < st->tol)
-              st->status[k] = kConverged;
-            else if (it >= st->max_iterations)
-              st->status[k] = kCap;
-            else
-              st->f_prev[k] = f;
+        ++st->iters[k];
+        double e = st->sqnorm + msq - 2.0 * inner;
+        e = e > 0.0 ? e : 0.0;  // als.py:114-115 (NaN clamps to 0 as there)
+        if (st->ls_enabled)
+          st->e_tmp[k] = e;  // decided after the line-search candidate (ls_finish)
+        else
+          decide_model(st, k, e);
+      }
+      __syncthreads();
+    }
+  }
+}
+
+// ------------------------------------------------------------- line search --
+// Candidate point prev + alpha (curr - prev) for every model holding a
+// snapshot (extrapolate_factors, als.py:137-138: evaluated as
+// p + alpha * (c - p) with three roundings, no FMA contraction) and its
+// Gramians; models without a snapshot or with a non-finite error skip.
+__global__ void __launch_bounds__(kUpdThreads) ls_candidate_kernel(EngState* st) {
+  extern __shared__ __align__(16) double dsm[];
+  const int N = st->order;
+  const long long ld = st->ld;
+  for (int slot = blockIdx.x; slot < st->n_active; slot += gridDim.x) {
+    const int k = st->slot_model[slot];
+    const int R = st->rank[k];
+    const int off = st->slot_off[slot];
+    const bool act = !st->failed[k] && st->has_snap[k] && isfinite(st->e_tmp[k]);
+    if (threadIdx.x == 0) st->ls_act[k] = act ? 1 : 0;
+    if (!act) continue;
+    const double alpha =
+        st->ls_alpha > 0.0 ? st->ls_alpha : pow((double)st->iters[k], 1.0 / 3.0);
+    for (int n = 0; n < N; ++n) {
+      const int rows = (int)st->dims[n];
+      for (long long e = threadIdx.x; e < (long long)rows * R; e += blockDim.x) {
+        const long long i = e / R;
+        const long long at = i * ld + off + (e - i * R);
+        const double p = st->S[n][at], c = st->F[n][at];
+        st->Cb[n][at] = __dadd_rn(p, __dmul_rn(alpha, __dsub_rn(c, p)));
+      }
+    }
+    __syncthreads();
+    for (int n = 0; n < N; ++n) {
+      double* G = st->cgrams + n * st->gram_stride + st->gram_off[k];
+      if (R <= kFastR)
+        block_gram_fast(st->Cb[n] + off, ld, (int)st->dims[n], R, dsm, G);
+      else
+        block_gram(st->Cb[n], ld, off, (int)st->dims[n], R, G);
+    }
+    __syncthreads();
+  }
+}
+
+// Candidate error from the fresh last-mode MTTKRP of the candidates (Mout),
+// keep the better point (driver.py:255-259), then the stopping rule and the
+// snapshot of a continuing model (driver.py:271-273).
+__global__ void __launch_bounds__(kUpdThreads) ls_finish_kernel(EngState* st) {
+  __shared__ double red[kUpdThreads];
+  __shared__ int accept;
+  const int N = st->order;
+  const long long ld = st->ld;
+  const int n = N - 1;
+  for (int slot = blockIdx.x; slot < st->n_active; slot += gridDim.x) {
+    const int k = st->slot_model[slot];
+    const int R = st->rank[k];
+    const int off = st->slot_off[slot];
+    const long long go = st->gram_off[k];
+    double e = st->e_tmp[k];
+    if (st->ls_act[k]) {
+      const int rows = (int)st->dims[n];
+      double part = 0.0;
+      for (long long el = threadIdx.x; el < (long long)rows * R; el += blockDim.x) {
+        const long long i = el / R;
+        const long long at = i * ld + off + (el - i * R);
+        part = fma(st->Cb[n][at], st->Mout[at], part);
+      }
+      const double inner = block_sum(part, red);
+      double mp = 0.0;
+      for (int idx = threadIdx.x; idx < R * R; idx += blockDim.x) {
+        double h = st->cgrams[go + idx];
+        for (int i = 1; i < N; ++i) h *= st->cgrams[i * st->gram_stride + go + idx];
+        mp += h;
+      }
+      const double msq = block_sum(mp, red);
+      double ec = st->sqnorm + msq - 2.0 * inner;
+      ec = ec > 0.0 ? ec : 0.0;
+      if (threadIdx.x == 0) accept = ec < e ? 1 : 0;
+      __syncthreads();
+      if (accept) {
+        e = ec;
+        for (int m = 0; m < N; ++m) {
+          const int rm = (int)st->dims[m];
+          for (long long el = threadIdx.x; el < (long long)rm * R; el += blockDim.x) {
+            const long long i = el / R;
+            const long long at = i * ld + off + (el - i * R);
+            st->F[m][at] = st->Cb[m][at];
           }
+          for (int idx = threadIdx.x; idx < R * R; idx += blockDim.x)
+            st->grams[m * st->gram_stride + go + idx] = st->cgrams[m * st->gram_stride + go + idx];
         }
       }
       __syncthreads();
     }
+    if (threadIdx.x == 0) decide_model(st, k, e);
+    __syncthreads();
+    if (st->status[k] == kActive) {
+      // continuing: snapshot the (possibly extrapolated) iterate
+      for (int m = 0; m < N; ++m) {
+        const int rm = (int)st->dims[m];
+        for (long long el = threadIdx.x; el < (long long)rm * R; el += blockDim.x) {
+          const long long i = el / R;
+          const long long at = i * ld + off + (el - i * R);
+          st->S[m][at] = st->F[m][at];
+        }
+      }
+      if (threadIdx.x == 0) st->has_snap[k] = 1;
+    }
+    __syncthreads();
   }
 }
 
@@ -316,6 +443,7 @@ __global__ void engine_plan_kernel(EngState* st) {
       const int k = head++;
       st->status[k] = kActive;
       st->fresh[k] = 1;
+      if (st->has_snap) st->has_snap[k] = 0;
       st->t_admit[k] = now;
       st->slot_model[new_n] = k;
       st->slot_off[new_n] = new_w;
@@ -360,18 +488,21 @@ __global__ void engine_move_kernel(EngState* st) {
   if (total == 0) return;
   extern __shared__ __align__(16) double row[];
   const int N = st->order;
-  long long rows_total = 0;
-  for (int n = 0; n < N; ++n) rows_total += st->dims[n];
+  long long rows_f = 0;
+  for (int n = 0; n < N; ++n) rows_f += st->dims[n];
+  // line search: the snapshot rows travel with the factor rows (KEEP only)
+  const long long rows_total = st->ls_enabled ? 2 * rows_f : rows_f;
   const int ow = st->old_width;
   const int nm = st->n_moves;
   for (long long gr = blockIdx.x; gr < rows_total; gr += gridDim.x) {
+    const bool snap = gr >= rows_f;
     int n = 0;
-    long long i = gr;
+    long long i = snap ? gr - rows_f : gr;
     while (i >= st->dims[n]) {
       i -= st->dims[n];
       ++n;
     }
-    double* F = st->F[n] + i * st->ld;
+    double* F = (snap ? st->S[n] : st->F[n]) + i * st->ld;
     for (int c = threadIdx.x; c < ow; c += blockDim.x) row[c] = F[c];
     __syncthreads();
     for (int e = threadIdx.x; e < total; e += blockDim.x) {
@@ -384,6 +515,7 @@ __global__ void engine_move_kernel(EngState* st) {
       const int k = st->mv_model[lo];
       const int R = st->rank[k];
       const long long po = st->pool_off[(long long)k * N + n] + i * R + r;
+      if (snap && st->mv_kind[lo] != kMoveKeep) continue;
       switch (st->mv_kind[lo]) {
         case kMoveKeep: F[st->mv_dst[lo] + r] = row[st->mv_src[lo] + r]; break;
         case kMoveRetire: st->pool[po] = row[st->mv_src[lo] + r]; break;
@@ -463,6 +595,8 @@ struct Engine {
   int tree_variant = 0;
   double* d_partial = nullptr;
   double* d_ones = nullptr;
+  void* d_ls = nullptr;  // line-search buffers (allocated on first enable)
+  size_t ls_smem = 0;
   int upd_grid = 0, upd_nthr = 0, upd_rb = 0;
   UpdateKernel upd_kernel = nullptr;
   size_t upd_smem = 0, move_smem = 0;
@@ -526,6 +660,7 @@ static int engine_free(Engine* e) {
   if (e->d_ws) cudaFree(e->d_ws);
   if (e->d_partial) cudaFree(e->d_partial);
   if (e->d_ones) cudaFree(e->d_ones);
+  if (e->d_ls) cudaFree(e->d_ls);
   if (e->d_st) cudaFree(e->d_st);
   if (e->h_done) cudaFreeHost(e->h_done);
   delete e;
@@ -704,6 +839,7 @@ static int engine_reset(Engine* e, double tol, int max_iterations, double sqnorm
   CALS_CUDA_TRY(cudaMemsetAsync(h.iters, 0, nm * 4, stream));
   CALS_CUDA_TRY(cudaMemsetAsync(h.failed, 0, nm * 4, stream));
   CALS_CUDA_TRY(cudaMemsetAsync(h.fresh, 0, nm * 4, stream));
+  if (h.has_snap) CALS_CUDA_TRY(cudaMemsetAsync(h.has_snap, 0, nm * 4, stream));
   CALS_CUDA_TRY(cudaMemsetAsync(h.retire_seq, 0xff, nm * 4, stream));
   std::vector<double> minf(nm, -INFINITY), pinf(nm, INFINITY);
   // f_prev = -inf, err = +inf, fit = -inf (driver.py:56-67)
@@ -770,13 +906,76 @@ static int enqueue_plan(Engine* e, cudaStream_t stream) {
   return kOk;
 }
 
+// Line search: candidates + their Gramians, ONE fused last-mode MTTKRP over
+// every candidate at once (the reference runs one single-instance MTTKRP per
+// model, driver.py:252-254), then accept / stopping rule / snapshot.
+static int enqueue_line_search(Engine* e, cudaStream_t stream) {
+  const int N = e->order;
+  ls_candidate_kernel<<<e->upd_grid, kUpdThreads, e->ls_smem, stream>>>(e->d_st);
+  CALS_CUDA_TRY(cudaGetLastError());
+  FactorSet fs{};
+  for (int n = 0; n < N; ++n) fs.ptr[n] = e->h_st.Cb[n];
+  fs.ld = e->ld;
+  int rc = launch_mttkrp(*e->t, N - 1, fs, 0, &e->d_st->width, e->capacity, e->h_st.Mout, e->ld,
+                         e->d_ws, e->ws_bytes, e->variants[N - 1], stream);
+  if (rc) return rc;
+  ls_finish_kernel<<<e->upd_grid, kUpdThreads, 0, stream>>>(e->d_st);
+  CALS_CUDA_TRY(cudaGetLastError());
+  return kOk;
+}
+
 static int enqueue_iteration(Engine* e, cudaStream_t stream) {
   for (int n = 0; n < e->order; ++n) {
     int rc = enqueue_mode_mttkrp(e, n, stream);
     if (!rc) rc = enqueue_mode_update(e, n, stream);
     if (rc) return rc;
   }
+  if (e->h_st.ls_enabled) {
+    int rc = enqueue_line_search(e, stream);
+    if (rc) return rc;
+  }
   return enqueue_plan(e, stream);
+}
+
+static int engine_set_line_search(Engine* e, int enabled, double alpha) {
+  EngState& h = e->h_st;
+  if (enabled && !e->d_ls) {
+    const int N = e->order;
+    const size_t nm = std::max(1, e->n_models);
+    size_t total = 0;
+    std::vector<std::pair<void**, size_t>> items;
+    for (int n = 0; n < N; ++n) {
+      items.push_back({(void**)&h.S[n], size_t(e->t->dims[n]) * e->ld * 8});
+      items.push_back({(void**)&h.Cb[n], size_t(e->t->dims[n]) * e->ld * 8});
+    }
+    items.push_back({(void**)&h.cgrams, size_t(N) * e->gram_stride * 8});
+    items.push_back({(void**)&h.has_snap, nm * 4});
+    items.push_back({(void**)&h.ls_act, nm * 4});
+    items.push_back({(void**)&h.e_tmp, nm * 8});
+    for (auto& it : items) total = align_up(total, 256) + it.second;
+    CALS_CUDA_TRY(cudaMalloc(&e->d_ls, total));
+    CALS_CUDA_TRY(cudaMemset(e->d_ls, 0, total));
+    size_t off = 0;
+    for (auto& it : items) {
+      off = align_up(off, 256);
+      *it.first = static_cast<char*>(e->d_ls) + off;
+      off += it.second;
+    }
+    e->ls_smem = size_t(kUpdThreads) * (kFastR + 1) * 8;
+    CALS_CUDA_TRY(cudaFuncSetAttribute(ls_candidate_kernel,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)e->ls_smem));
+  }
+  if (h.ls_enabled != enabled || (enabled && h.ls_alpha != alpha)) {
+    // the captured iteration graph depends on the line-search setting
+    if (e->exec) cudaGraphExecDestroy(e->exec);
+    if (e->graph) cudaGraphDestroy(e->graph);
+    e->exec = nullptr;
+    e->graph = nullptr;
+  }
+  h.ls_enabled = enabled ? 1 : 0;
+  h.ls_alpha = alpha;
+  return kOk;
 }
 
 static int engine_capture(Engine* e, cudaStream_t stream) {
@@ -1051,6 +1250,13 @@ int cals_engine_trace(cals_engine* e, int32_t* widths, int32_t* n_active, double
   return kOk;
 }
 
+int cals_engine_set_line_search(cals_engine* e, int enabled, double alpha) {
+  CALS_CHECK(e, kErrInvalid, "null engine");
+  CALS_CHECK(!enabled || alpha <= 0.0 || alpha > 1.0, kErrInvalid,
+             "extrapolation alpha must be > 1 (or <= 0 for the i^(1/3) rule)");
+  return engine_set_line_search(e->e, enabled, alpha);
+}
+
 // ---- step-wise driving (host-orchestrated loops, e.g. the mode-0-sharded
 // configuration with an all-reduce between the MTTKRP and the update) ------
 int cals_engine_begin(cals_engine* e, double tol, int max_iterations, double sqnorm,
@@ -1059,6 +1265,8 @@ int cals_engine_begin(cals_engine* e, double tol, int max_iterations, double sqn
   CALS_CHECK(max_iterations >= 1, kErrInvalid, "max_iterations must be >= 1");
   CALS_CHECK(sqnorm > 0.0, kErrInvalid, "tensor squared norm must be positive");
   Engine* g = e->e;
+  CALS_CHECK(!g->h_st.ls_enabled, kErrUnsupported,
+             "line search is not supported by the step-wise (sharded) driver");
   cudaStream_t s = (cudaStream_t)stream;
   int rc = engine_reset(g, tol, max_iterations, sqnorm, s);
   if (rc) return rc;

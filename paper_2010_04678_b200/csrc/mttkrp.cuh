@@ -73,7 +73,9 @@ struct TileCfg {
   static constexpr int B_ELEMS = kBK * (BN + kPad);
   static constexpr int STAGES = 4;
   static constexpr size_t kStageBytes = size_t(A_ELEMS + B_ELEMS) * 8;
-  static constexpr size_t kSmemBytes = STAGES * kStageBytes + 2 * STAGES * 8 + 128;
+  static constexpr size_t kAccBytes = size_t(kConsumerWarps) * 32 * MI * NI * 2 * 8;
+  static constexpr size_t kBarBytes = 2 * STAGES * 8;
+  static constexpr size_t kSmemBytes = STAGES * kStageBytes + kBarBytes + kAccBytes + 128;
 };
 
 // p-tile `pt` loads the kBK-wide box at p0 and consumes its k4 steps
@@ -101,9 +103,9 @@ __device__ __forceinline__ void unit_decode(int u, int tm, int tn, int& tile_m, 
 }
 
 template <int MI, int NI, int WM, int WN, bool KC>
-// 2 CTAs x 5 warps per SM fit 200 registers per thread (per-warp allocation);
-// __launch_bounds__(.., 2) alone makes ptxas assume 6-warp granularity (168).
-__global__ void __maxnreg__(200)
+// 2 CTAs x 5 warps per SM: some SMSP holds 3 warps, and each SMSP's register
+// file is 16K 32-bit registers -> at most 168 registers per thread.
+__global__ void __launch_bounds__(TileCfg<MI, NI, WM, WN>::kThreads, 2)
     mttkrp_dmma_kernel(const __grid_constant__ CUtensorMap tmA,
                        const __grid_constant__ CUtensorMap tmB, const MttkrpArgs args) {
   using C = TileCfg<MI, NI, WM, WN>;
@@ -172,6 +174,8 @@ __global__ void __maxnreg__(200)
 
   // ======================= DMMA consumers =====================================
   const int wm = warp / WN, wn = warp % WN;
+  double* accs = reinterpret_cast<double*>(smem_raw + STAGES * C::kStageBytes + C::kBarBytes) +
+                 size_t(warp) * (MI * NI * 2) * 32 + lane;
   const int r = lane >> 2, kq = lane & 3;
   int stage = 0;
   uint32_t phase = 0;
@@ -183,28 +187,21 @@ __global__ void __maxnreg__(200)
     const int m0 = tile_m * BM, c0 = tile_n * BN;
     const int cw = c0 + wn * 8 * NI + 2 * kq;  // this lane's first column
 
-    double acc[MI][NI][2];
+    // The cross-slab accumulator lives in shared memory (this lane's column
+    // of a per-warp [element][lane] block): it is touched once per q-slab,
+    // and keeping it out of registers leaves the whole register budget to
+    // the DMMA tile and its pipelined fragments.
 #pragma unroll
-    for (int i = 0; i < MI; ++i)
-#pragma unroll
-      for (int j = 0; j < NI; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+    for (int e = 0; e < MI * NI * 2; ++e) accs[e * 32] = 0.0;
 
     for (int q = qb; q < qe; ++q) {
-      double hi[NI][2];
-      const double* hrow = args.hi + (long long)q * args.ldh;
-#pragma unroll
-      for (int j = 0; j < NI; ++j) {
-        const int c = cw + 8 * j;
-        hi[j][0] = c < W ? __ldg(hrow + c) : 0.0;
-        hi[j][1] = c + 1 < W ? __ldg(hrow + c + 1) : 0.0;
-      }
       double t[MI][NI][2];
 #pragma unroll
       for (int i = 0; i < MI; ++i)
 #pragma unroll
         for (int j = 0; j < NI; ++j) t[i][j][0] = t[i][j][1] = 0.0;
 
-      for (int pt = 0; pt < np; ++pt) {
+      auto run_stage = [&](int pt) {
         mbar_wait(&full[stage], phase);
         const double* sa = smem + size_t(stage) * (C::A_ELEMS + C::B_ELEMS);
         const double* sb = sa + C::A_ELEMS;
@@ -240,7 +237,19 @@ __global__ void __maxnreg__(200)
         __syncwarp();
         if (lane == 0) mbar_arrive(&empty[stage]);
         if (++stage == STAGES) { stage = 0; phase ^= 1u; }
+      };
+      for (int pt = 0; pt < np - 1; ++pt) run_stage(pt);
+      // Hi[q] is only live across the last p-tile (its latency hides behind
+      // that tile's DMMAs) -- keeps the main loop within the register budget
+      double hi[NI][2];
+      const double* hrow = args.hi + (long long)q * args.ldh;
+#pragma unroll
+      for (int j = 0; j < NI; ++j) {
+        const int c = cw + 8 * j;
+        hi[j][0] = c < W ? __ldg(hrow + c) : 0.0;
+        hi[j][1] = c + 1 < W ? __ldg(hrow + c + 1) : 0.0;
       }
+      run_stage(np - 1);
       if (args.side) {
         // dimension-tree partial: the unscaled slab product, written once
 #pragma unroll
@@ -263,8 +272,9 @@ __global__ void __maxnreg__(200)
       for (int i = 0; i < MI; ++i)
 #pragma unroll
         for (int j = 0; j < NI; ++j) {
-          acc[i][j][0] = fma(t[i][j][0], hi[j][0], acc[i][j][0]);
-          acc[i][j][1] = fma(t[i][j][1], hi[j][1], acc[i][j][1]);
+          double* a2 = accs + ((i * NI + j) * 2) * 32;
+          a2[0] = fma(t[i][j][0], hi[j][0], a2[0]);
+          a2[32] = fma(t[i][j][1], hi[j][1], a2[32]);
         }
     }
 
@@ -277,10 +287,11 @@ __global__ void __maxnreg__(200)
 #pragma unroll
       for (int j = 0; j < NI; ++j) {
         const int c = cw + 8 * j;
+        const double* a2 = accs + ((i * NI + j) * 2) * 32;
         if (c + 1 < W) {
-          *reinterpret_cast<double2*>(orow + c) = make_double2(acc[i][j][0], acc[i][j][1]);
+          *reinterpret_cast<double2*>(orow + c) = make_double2(a2[0], a2[32]);
         } else if (c < W) {
-          orow[c] = acc[i][j][0];
+          orow[c] = a2[0];
         }
       }
     }

@@ -66,17 +66,17 @@ def run(t: DenseTensor, models: Iterable[Model], cfg: ConvergenceConfig, *,
                 raise CapacityError(f"model {m.id!r} rank {m.rank} exceeds r_star {r_star}")
     if mode not in (ExecutionMode.SEQUENTIAL, ExecutionMode.PARALLEL, ExecutionMode.CALS):
         raise ValueError(f"unknown execution mode {mode!r}")
-    if ls.enabled or nonneg:
+    if nonneg:
         raise NotImplementedError(_NEXT)
     if not queue:
         return []
     if t.sqnorm <= 0.0:
         raise ValueError("tensor squared norm must be positive")
     if mode is ExecutionMode.CALS:
-        return _run_fused(t, queue, cfg, r_star, trace, label_per_model=False)
+        return _run_fused(t, queue, cfg, r_star, trace, label_per_model=False, ls=ls)
     out = []
     for m in queue:
-        out += _run_fused(t, [m], cfg, m.rank, trace, label_per_model=True)
+        out += _run_fused(t, [m], cfg, m.rank, trace, label_per_model=True, ls=ls)
     return out
 
 
@@ -85,11 +85,14 @@ def _instance_flops(t: DenseTensor, rank: int, iterations: int) -> int:
 
 
 def _run_fused(t: DenseTensor, queue: list[Model], cfg: ConvergenceConfig, r_star: int,
-               trace: list | None, label_per_model: bool) -> list[Model]:
+               trace: list | None, label_per_model: bool,
+               ls: LineSearchConfig | None = None) -> list[Model]:
     dev = t.device()
     eng = CalsEngine(dev, r_star, [m.rank for m in queue],
                      trace_capacity=_trace_cap(queue, cfg) if trace is not None else 1)
     try:
+        if ls is not None and ls.enabled:
+            eng.set_line_search(True, ls.alpha)
         eng.load_pool(eng.pack([m.factors for m in queue]))
         tic = time.perf_counter()
         eng.run(cfg.tol, cfg.max_iterations, t.sqnorm)

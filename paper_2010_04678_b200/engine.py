@@ -137,6 +137,11 @@ class CalsEngine:
         n = min(cnt.value, cap)
         return [(int(w[i]), int(a[i]), float(sec[i])) for i in range(n)]
 
+    def set_line_search(self, enabled: bool, alpha: float | None = None):
+        """Line search after every iteration (alpha None -> iteration^(1/3))."""
+        _native.call("cals_engine_set_line_search", self.handle, 1 if enabled else 0,
+                     0.0 if alpha is None else float(alpha))
+
     # ------------------------------------------------------- step-wise
     def begin(self, tol: float, max_iterations: int, sqnorm: float, stream=None):
         import torch

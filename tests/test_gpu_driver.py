@@ -161,6 +161,34 @@ def test_eem_shape_refill_vs_oracle(cals):
         assert abs(m.fit - r.fit) <= 1e-6
 
 
+def _run_ls_and_compare(cals, name, t, models, tol, iters, r_star, alpha, fac_tol=1e-9):
+    g = np.load(os.path.join(GOLDEN, f"run_{name}.npz"))
+    trace = []
+    out = cals.run(t, models, cals.ConvergenceConfig(tol=tol, max_iterations=iters), r_star=r_star,
+                   trace=trace, ls=cals.LineSearchConfig(enabled=True, alpha=alpha))
+    assert [m.id for m in out] == [str(s) for s in g["order"]]
+    assert [m.status.value for m in out] == [str(s) for s in g["status"]]
+    assert [m.iterations_done for m in out] == g["iterations"].tolist()
+    assert [s.meta["width"] for s in trace] == g["widths"].tolist()
+    for m, f in zip(out, g["fit"]):
+        assert abs(m.fit - f) <= 1e-6
+        for n in range(t.order):
+            assert rel(m.factors[n], g[f"{m.id}_f{n}"]) <= fac_tol, (m.id, n)
+
+
+def test_line_search_matches_reference(cals):
+    """driver.py:250-259 with the i^(1/3) rule and a constant alpha; one fused
+    candidate MTTKRP per iteration on the GPU."""
+    t = cals.generate_synthetic((12, 10, 8), 3, 0.1, seed=0)
+    _run_ls_and_compare(cals, "ls_cube_root", t, cals.build_models(t.dims, [1, 2, 3, 4], 2, seed=1),
+                        0.0, 8, 20, None)
+    _run_ls_and_compare(cals, "ls_const", t, cals.build_models(t.dims, [2, 3], 2, seed=7),
+                        0.0, 8, 6, 1.5)
+    t = cals.generate_synthetic((50, 50, 50), 5, 0.1, seed=0)
+    _run_ls_and_compare(cals, "ls_c1_tol", t, cals.build_models(t.dims, [1, 2, 3, 4, 5], 4, seed=1),
+                        1e-6, 1000, 60, None, fac_tol=1e-6)
+
+
 @pytest.mark.parametrize("tree", ["0", "1", "2"])
 def test_dimension_tree_variants_match_reference(cals, tree, monkeypatch):
     """The engine's dimension-tree schedules (none / Y = X x3 A2 shared by

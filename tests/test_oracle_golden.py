@@ -103,6 +103,19 @@ def test_run_c1():
     _check_run("c1_tol", dims, data, O.build_models(dims, [1, 2, 3, 4, 5], 4, seed=1), 1e-6, 1000, 60)
 
 
+def test_run_line_search():
+    dims, data = O.generate_synthetic((12, 10, 8), 3, 0.1, seed=0)
+    for name, ranks, seed, r_star, alpha in [("ls_cube_root", [1, 2, 3, 4], 1, 20, None),
+                                             ("ls_const", [2, 3], 7, 6, 1.5)]:
+        g = load(f"run_{name}.npz")
+        out = O.run_cals(data, dims, O.build_models(dims, ranks, 2, seed=seed), 0.0, 8, r_star,
+                         ls=True, ls_alpha=alpha)
+        assert [r.id for r in out] == [str(s) for s in g["order"]]
+        for r in out:
+            for n in range(3):
+                assert rel(r.factors[n], g[f"{r.id}_f{n}"]) <= 1e-9
+
+
 def test_run_other_orders_and_failure():
     dims, data = O.generate_synthetic((9, 7), 2, 0.05, seed=3)
     _check_run("order2", dims, data, O.build_models(dims, [1, 2, 3], 2, seed=4), 0.0, 6, 12)
