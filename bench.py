@@ -261,7 +261,9 @@ def main_gpu(args) -> None:
     gpu_launches = iters_launched * (3 * 3 + 2) + 2
 
     # ---- e2e through the public API with host buffers
-    e2e_times = []
+    from paper_2010_04678_b200.driver import LAST_RUN_PROFILE
+
+    e2e_times, phases = [], []
     h2d = t.data.nbytes + pool_host.nbytes
     d2h = pool_host.nbytes + n_models * (4 * 3 + 8 * 3) + 8 * sum(m.rank for m in models)
     for i in range(args.warmup + max(2, min(args.steps, 5))):
@@ -273,6 +275,7 @@ def main_gpu(args) -> None:
         torch.cuda.synchronize()
         if i >= args.warmup:
             e2e_times.append(time.perf_counter() - tic)
+            phases.append(dict(LAST_RUN_PROFILE))
         tt.release_device()
         assert len(out) == n_models
     e2e_sec = float(np.mean(e2e_times))
@@ -280,7 +283,8 @@ def main_gpu(args) -> None:
     if world > 1:
         dist.all_reduce(te, op=dist.ReduceOp.MAX)
     e2e = {"value": n_models * world / float(te.item()), "unit": "models/s",
-           "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h)}
+           "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
+           "phases_ms": {k: 1e3 * float(np.mean([p[k] for p in phases])) for k in phases[0]}}
 
     # ---- roofline of the fused MTTKRP kernel at W = 2100
     peak = C.c_double()

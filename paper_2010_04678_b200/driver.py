@@ -25,6 +25,10 @@ from .multimatrix import DEFAULT_R_STAR, CapacityError
 from .tensor import DenseTensor
 
 
+# host-side phase timings of the most recent fused run (diagnostics / bench)
+LAST_RUN_PROFILE: dict = {}
+
+
 class ExecutionMode(enum.Enum):
     SEQUENTIAL = "sequential"
     PARALLEL = "parallel"
@@ -87,20 +91,29 @@ def _instance_flops(t: DenseTensor, rank: int, iterations: int) -> int:
 def _run_fused(t: DenseTensor, queue: list[Model], cfg: ConvergenceConfig, r_star: int,
                trace: list | None, label_per_model: bool,
                ls: LineSearchConfig | None = None) -> list[Model]:
+    prof = LAST_RUN_PROFILE
+    prof.clear()
+    t0 = time.perf_counter()
     dev = t.device()
+    t1 = time.perf_counter()
     eng = CalsEngine(dev, r_star, [m.rank for m in queue],
                      trace_capacity=_trace_cap(queue, cfg) if trace is not None else 1)
+    t2 = time.perf_counter()
     try:
         if ls is not None and ls.enabled:
             eng.set_line_search(True, ls.alpha)
         eng.load_pool(eng.pack([m.factors for m in queue]))
         tic = time.perf_counter()
         eng.run(cfg.tol, cfg.max_iterations, t.sqnorm)
+        t4 = time.perf_counter()
         res = eng.results()
         wall = time.perf_counter() - tic
         records = eng.trace() if (trace is not None and not label_per_model) else None
     finally:
         eng.close()
+    t5 = time.perf_counter()
+    prof.update(tensor_upload_s=t1 - t0, engine_create_s=t2 - t1, pool_upload_s=tic - t2,
+                device_loop_s=t4 - tic, results_download_s=t5 - t4)
     for m in queue:
         m.status = ModelStatus.ACTIVE
     order = np.argsort(res.retire_seq, kind="stable")
@@ -115,6 +128,7 @@ def _run_fused(t: DenseTensor, queue: list[Model], cfg: ConvergenceConfig, r_sta
                          error=float(res.error[k]), fit=float(res.fit[k]),
                          iterations_done=int(res.iterations[k]), status=status,
                          seconds_active=float(res.seconds_active[k]), meta=meta))
+    prof["build_models_s"] = time.perf_counter() - t5
     if trace is not None:
         if label_per_model:
             for r in out:
