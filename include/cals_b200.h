@@ -113,6 +113,22 @@ int cals_engine_variant(cals_engine* e, int mode, int* variant, int* bm, int* bn
  * replaces the iterate.  Takes effect at the next cals_engine_run. */
 int cals_engine_set_line_search(cals_engine* e, int enabled, double alpha);
 
+/* Non-negative updates (replaces als.py:185-278 nnls_solve_row /
+ * nnls_update as called from driver.py:226-227): every factor row is fitted
+ * by a warm-started Lawson-Hanson active-set search (one warp per row, ranks
+ * <= 32), the active sets persisting per model / mode / row across
+ * iterations.  cals_engine_nnls_warnings reports per model whether a row hit
+ * the 3R iteration cap (NonConvergedNnlsWarning, als.py:70-71). */
+int cals_engine_set_nonneg(cals_engine* e, int enabled);
+/* Operator level (replaces als.py:185-278 for one block): x[i] = argmin
+ * x^T h x - 2 m[i]^T x, x >= 0, warm-started from active[i] (bit a set =
+ * variable a pinned to zero; updated in place); converged[i] = 0 when the
+ * max_iter cap (< 0: 3 * rank) was hit.  rank <= 32. */
+int cals_nnls_rows(int rows, int rank, const double* m, int64_t ldm, const double* h,
+                   uint32_t* active, double* x, int64_t ldx, int32_t* converged, int max_iter,
+                   void* stream);
+int cals_engine_nnls_warnings(cals_engine* e, int32_t* flags);
+
 /* Step-wise driving of the same loop (what cals_engine_run replays as a CUDA
  * graph), for host-orchestrated runs that interleave collectives: the
  * mode-0-sharded configuration all-reduces the partial MTTKRP of modes >= 1

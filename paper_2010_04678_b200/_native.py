@@ -54,6 +54,11 @@ SIGNATURES = {
     "cals_engine_variant": (C.c_int, [C.c_void_p, C.c_int, c_int_p, c_int_p, c_int_p, c_int_p]),
     "cals_fp64_peak_probe": (C.c_int, [C.c_void_p, c_dbl_p]),
     "cals_engine_set_line_search": (C.c_int, [C.c_void_p, C.c_int, C.c_double]),
+    "cals_engine_set_nonneg": (C.c_int, [C.c_void_p, C.c_int]),
+    "cals_nnls_rows": (C.c_int, [C.c_int, C.c_int, C.c_void_p, C.c_int64, C.c_void_p,
+                                 C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p, C.c_int,
+                                 C.c_void_p]),
+    "cals_engine_nnls_warnings": (C.c_int, [C.c_void_p, C.c_void_p]),
     "cals_engine_begin":(C.c_int, [C.c_void_p, C.c_double, C.c_int, C.c_double, C.c_void_p]),
     "cals_engine_enqueue_mttkrp": (C.c_int, [C.c_void_p, C.c_int, C.c_void_p]),
     "cals_engine_enqueue_update": (C.c_int, [C.c_void_p, C.c_int, C.c_void_p]),

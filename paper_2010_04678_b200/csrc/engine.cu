@@ -21,6 +21,11 @@
 #include "internal.h"
 #include "mttkrp.cuh"
 #include "update.cuh"
+#include "nnls.cuh"
+
+namespace cals {
+constexpr int kNnlsWs = kNnlsP * 32 + 32 + 32 * 32;  // per-warp NNLS scratch (doubles)
+}
 
 namespace cals {
 
@@ -86,6 +91,12 @@ struct EngState {
   int* has_snap;
   int* ls_act;
   double* e_tmp;
+  // non-negative updates (als.py:185-278): per model, mode and factor row
+  // the active-set bitmask carried between iterations
+  int nonneg;
+  unsigned* nnls_state;
+  const long long* nnls_off;  // [k * order + n]
+  int* nnls_warn;             // a row hit the active-set iteration cap
 };
 
 // Stopping rule for model k with squared error e (driver.py:260-273); the
@@ -150,6 +161,13 @@ __global__ void __launch_bounds__(kUpdThreads) engine_update_kernel(EngState* st
         else
           block_gram(st->F[i], ld, off, (int)st->dims[i], R, gram(i));
       }
+      if (st->nonneg) {  // NnlsState(t.dims, rank): nothing pinned (driver.py:206)
+        for (int i = 0; i < N; ++i) {
+          unsigned* sp = st->nnls_state + st->nnls_off[(long long)k * N + i];
+          for (long long r = threadIdx.x; r < st->dims[i]; r += blockDim.x) sp[r] = 0u;
+        }
+        if (threadIdx.x == 0) st->nnls_warn[k] = 0;
+      }
       __syncthreads();
       if (threadIdx.x == 0) st->fresh[k] = 0;
     }
@@ -204,8 +222,31 @@ __global__ void __launch_bounds__(kUpdThreads) engine_update_kernel(EngState* st
         __syncthreads();
       } else {
         bool done = false;
+        if (st->nonneg) {
+          // non-negative update (driver.py:226-227 -> nnls_update): one warp
+          // per factor row, warm-started active sets kept per row
+          for (int idx = threadIdx.x; idx < R * R; idx += blockDim.x) H[idx] = Hsave[idx];
+          __syncthreads();
+          const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+          double* Ws = X + warp * kNnlsWs;
+          unsigned* state = st->nnls_state + st->nnls_off[(long long)k * N + n];
+          for (int i = warp; i < rows; i += blockDim.x >> 5) {
+            const double f = lane < R ? Mb[(long long)i * ld + lane] : 0.0;
+            unsigned act = state[i];
+            bool conv = true;
+            const double x = nnls_row(H, R, f, &act, &conv, Ws);
+            if (lane < R) st->F[n][(long long)i * ld + off + lane] = x;
+            if (lane == 0) {
+              state[i] = act;
+              if (!conv) st->nnls_warn[k] = 1;
+            }
+          }
+          __syncthreads();
+          block_gram_fast(st->F[n] + off, ld, rows, R, X, gram(n));
+          done = true;
+        }
         if constexpr (RB > 0) {
-          chol_ok = flag != 0;
+          chol_ok = !done && flag != 0;
           if (chol_ok) {
             done = block_solve_gram_fast(H, inv_diag, R, Mb, ld, rows, st->F[n] + off, ld, X,
                                          gram(n), n == N - 1, &inner, red, true);
@@ -596,6 +637,7 @@ struct Engine {
   double* d_partial = nullptr;
   double* d_ones = nullptr;
   void* d_ls = nullptr;  // line-search buffers (allocated on first enable)
+  void* d_nnls = nullptr;  // NNLS active sets (allocated on first enable)
   size_t ls_smem = 0;
   int upd_grid = 0, upd_nthr = 0, upd_rb = 0;
   UpdateKernel upd_kernel = nullptr;
@@ -661,6 +703,7 @@ static int engine_free(Engine* e) {
   if (e->d_partial) cudaFree(e->d_partial);
   if (e->d_ones) cudaFree(e->d_ones);
   if (e->d_ls) cudaFree(e->d_ls);
+  if (e->d_nnls) cudaFree(e->d_nnls);
   if (e->d_st) cudaFree(e->d_st);
   if (e->h_done) cudaFreeHost(e->h_done);
   delete e;
@@ -935,6 +978,50 @@ static int enqueue_iteration(Engine* e, cudaStream_t stream) {
     if (rc) return rc;
   }
   return enqueue_plan(e, stream);
+}
+
+static int engine_set_nonneg(Engine* e, int enabled) {
+  EngState& h = e->h_st;
+  if (enabled) {
+    CALS_CHECK(e->max_rank <= kFastR, kErrUnsupported,
+               "non-negative updates support ranks up to 32");
+    if (!e->d_nnls) {
+      const int N = e->order;
+      const size_t nm = std::max(1, e->n_models);
+      std::vector<long long> offs(nm * N, 0);
+      long long at = 0;
+      for (int k = 0; k < e->n_models; ++k)
+        for (int n = 0; n < N; ++n) {
+          offs[(size_t)k * N + n] = at;
+          at += e->t->dims[n];
+        }
+      const size_t b_state = align_up(size_t(std::max<long long>(at, 1)) * 4, 256);
+      const size_t b_off = align_up(offs.size() * 8, 256);
+      CALS_CUDA_TRY(cudaMalloc(&e->d_nnls, b_state + b_off + nm * 4));
+      CALS_CUDA_TRY(cudaMemset(e->d_nnls, 0, b_state + b_off + nm * 4));
+      h.nnls_state = static_cast<unsigned*>(e->d_nnls);
+      h.nnls_off = reinterpret_cast<long long*>(static_cast<char*>(e->d_nnls) + b_state);
+      h.nnls_warn = reinterpret_cast<int*>(static_cast<char*>(e->d_nnls) + b_state + b_off);
+      CALS_CUDA_TRY(cudaMemcpy((void*)h.nnls_off, offs.data(), offs.size() * 8,
+                               cudaMemcpyHostToDevice));
+    }
+    const size_t need = size_t(e->max_rank) * e->max_rank * 8 +
+                        size_t(kUpdThreads / 32) * kNnlsWs * 8;
+    if (need > e->upd_smem) {
+      e->upd_smem = need;
+      CALS_CUDA_TRY(cudaFuncSetAttribute(e->upd_kernel,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)e->upd_smem));
+    }
+  }
+  if (h.nonneg != (enabled ? 1 : 0)) {
+    if (e->exec) cudaGraphExecDestroy(e->exec);
+    if (e->graph) cudaGraphDestroy(e->graph);
+    e->exec = nullptr;
+    e->graph = nullptr;
+  }
+  h.nonneg = enabled ? 1 : 0;
+  return kOk;
 }
 
 static int engine_set_line_search(Engine* e, int enabled, double alpha) {
@@ -1247,6 +1334,41 @@ int cals_engine_trace(cals_engine* e, int32_t* widths, int32_t* n_active, double
     if (n_active) n_active[i] = a[i];
     if (seconds) seconds[i] = (double)(tt[i + 1] - tt[i]) * 1e-9;
   }
+  return kOk;
+}
+
+int cals_nnls_rows(int rows, int rank, const double* m, int64_t ldm, const double* h,
+                   uint32_t* active, double* x, int64_t ldx, int32_t* converged, int max_iter,
+                   void* stream) {
+  CALS_CHECK(rows >= 0 && rank >= 1 && rank <= kFastR, kErrInvalid,
+             "rank must be in [1, 32] for the NNLS kernel");
+  CALS_CHECK(m && h && active && x && converged, kErrInvalid, "null argument");
+  if (rows == 0) return kOk;
+  const int warps = 4;
+  const size_t smem = (size_t(rank) * rank + size_t(warps) * kNnlsWs) * 8;
+  CALS_CUDA_TRY(cudaFuncSetAttribute(nnls_rows_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)smem));
+  const int blocks = std::max(1, std::min((rows + warps - 1) / warps, 148 * 8));
+  nnls_rows_kernel<<<blocks, 32 * warps, smem, (cudaStream_t)stream>>>(
+      rows, rank, m, ldm, h, active, x, ldx, converged, max_iter);
+  CALS_CUDA_TRY(cudaGetLastError());
+  return kOk;
+}
+
+int cals_engine_set_nonneg(cals_engine* e, int enabled) {
+  CALS_CHECK(e, kErrInvalid, "null engine");
+  return engine_set_nonneg(e->e, enabled);
+}
+
+int cals_engine_nnls_warnings(cals_engine* e, int32_t* flags) {
+  CALS_CHECK(e && flags, kErrInvalid, "null argument");
+  Engine* g = e->e;
+  if (!g->h_st.nnls_warn || g->n_models == 0) {
+    for (int k = 0; k < g->n_models; ++k) flags[k] = 0;
+    return kOk;
+  }
+  CALS_CUDA_TRY(cudaMemcpy(flags, g->h_st.nnls_warn, size_t(g->n_models) * 4,
+                           cudaMemcpyDeviceToHost));
   return kOk;
 }
 
