@@ -85,6 +85,9 @@ size_t cals_update_scratch_bytes(int rank);
 int cals_engine_create(cals_tensor* t, int r_star, int n_models, const int32_t* ranks,
                        int trace_capacity, cals_engine** out);
 int cals_engine_destroy(cals_engine* e);
+/* Re-bind an engine (and its device workspaces) to another tensor of the same
+ * shape, so repeated sweeps reuse every allocation. */
+int cals_engine_set_tensor(cals_engine* e, cals_tensor* t);
 int cals_engine_pool(cals_engine* e, double** pool, int64_t* elems);
 int cals_engine_load_pool(cals_engine* e, const double* src, int src_is_device, void* stream);
 /* Runs until every model has retired (ConvergenceConfig semantics,

@@ -183,6 +183,56 @@ def main() -> None:
     run_ls_case("ls_c1_tol", c1, build_models(c1.dims, [1, 2, 3, 4, 5], 4, seed=1),
                 1e-6, 1000, 60, None)
 
+    # non-negative updates (driver.py:226-227, als.py:185-278)
+    from cals.als import nnls_solve_row
+
+    def run_nn_case(name, tensor, models, tol, iters, r_star, ls_on=False):
+        trace: list = []
+        out = run(tensor, models, ConvergenceConfig(tol=tol, max_iterations=iters),
+                  mode=ExecutionMode.CALS, r_star=r_star, trace=trace, nonneg=True,
+                  ls=LineSearchConfig(enabled=ls_on))
+        d = {"order": np.array([m.id for m in out]),
+             "status": np.array([m.status.value for m in out]),
+             "iterations": np.array([m.iterations_done for m in out]),
+             "fit": np.array([m.fit for m in out]), "error": np.array([m.error for m in out]),
+             "widths": np.array([s.meta["width"] for s in trace]),
+             "n_active": np.array([s.meta["n_active"] for s in trace])}
+        for m in out:
+            for n, f in enumerate(m.factors):
+                d[f"{m.id}_f{n}"] = f
+        np.savez(os.path.join(OUT, f"run_{name}.npz"), **d)
+        meta["cases"][name] = {"dims": list(tensor.dims), "tol": tol, "max_iterations": iters,
+                               "r_star": r_star, "nonneg": True, "ls": ls_on}
+
+    run_nn_case("nn_fixed", small, build_models(small.dims, [1, 2, 3, 4], 2, seed=1), 0.0, 8, 20)
+    run_nn_case("nn_tol", small, build_models(small.dims, [2, 3], 2, seed=2), 1e-6, 300, 6)
+    rng = np.random.default_rng(67)
+    ldims = (6, 5, 4)
+    truth = [rng.random((d, 2)) for d in ldims]
+    lt = DenseTensor.from_array(np.einsum("ir,jr,kr->ijk", *truth))
+    lmodels = [Model.random(ldims, 2, rng, id=f"m{i}") for i in range(3)]
+    nn_in = {"data": lt.data.copy()}
+    for i, m in enumerate(lmodels):
+        for n in range(3):
+            nn_in[f"m{i}_f{n}"] = m.factors[n].copy()
+    np.savez(os.path.join(OUT, "nn_ls_inputs.npz"), **nn_in)
+    run_nn_case("nn_ls", lt, lmodels, 1e-7, 300, 6, ls_on=True)
+    rows = {}
+    rng = np.random.default_rng(99)
+    cnt = 0
+    for r in (1, 3, 8, 20):
+        for _ in range(12):
+            a = rng.standard_normal((r + 5, r))
+            h = a.T @ a
+            f = rng.standard_normal(r) * 2.0
+            act = rng.random(r) < 0.3
+            x, newact, conv = nnls_solve_row(h, f, act)
+            rows.update({f"p{cnt}_h": h, f"p{cnt}_f": f, f"p{cnt}_act": act, f"p{cnt}_x": x,
+                         f"p{cnt}_newact": newact, f"p{cnt}_conv": np.array(conv)})
+            cnt += 1
+    rows["n_cases"] = np.array(cnt)
+    np.savez(os.path.join(OUT, "nnls_rows.npz"), **rows)
+
     # failure isolation (test_driver.py:117-135)
     rng = np.random.default_rng(66)
     fd = (4, 4, 3)

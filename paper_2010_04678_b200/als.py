@@ -10,6 +10,7 @@ from __future__ import annotations
 
 import ctypes as C
 import math
+import warnings
 from dataclasses import dataclass
 from typing import Sequence
 
@@ -108,10 +109,6 @@ def fit_from_error(e: float, t_sqnorm: float) -> float:
     return 1.0 - math.sqrt(e) / math.sqrt(t_sqnorm)
 
 
-_NEXT = ("non-negative (NNLS) updates are the next row of the hot-path scope "
-         "(SURVEY.md section 8f) and are not implemented on the GPU yet")
-
-
 def extrapolate_factors(t, prev, curr, alpha: float, ws=None, variant_table=None):
     """Candidate ``prev + alpha * (curr - prev)``, its Gramians and exact
     error from a fresh last-mode MTTKRP on the GPU (als.py:127-144).  Inside
@@ -149,12 +146,54 @@ def line_search_step(prev, curr, cfg: LineSearchConfig, t, iteration: int | None
                  status=curr.status, meta=dict(curr.meta))
 
 
-def nnls_solve_row(*args, **kwargs):
-    raise NotImplementedError(_NEXT)
+def _nnls_rows_gpu(m: np.ndarray, h: np.ndarray, active: np.ndarray, max_iter: int):
+    """Run the warp-per-row Lawson-Hanson kernel (csrc/nnls.cuh) on a block."""
+    import torch
+
+    _native.load()
+    m = np.ascontiguousarray(m, dtype=np.float64)
+    rows, r = m.shape
+    if r > 32:
+        raise ValueError("the GPU NNLS kernel supports ranks up to 32")
+    bits = (np.asarray(active, dtype=bool) * (1 << np.arange(r, dtype=np.uint64))).sum(
+        axis=1).astype(np.uint32) if rows else np.zeros(0, np.uint32)
+    dev = torch.device("cuda", torch.cuda.current_device())
+    md = torch.from_numpy(m).to(dev)
+    hd = torch.from_numpy(np.ascontiguousarray(h, dtype=np.float64)).to(dev)
+    ad = torch.from_numpy(bits.view(np.int32).copy()).to(dev)
+    xd = torch.empty((max(rows, 1), r), dtype=torch.float64, device=dev)
+    cd = torch.empty(max(rows, 1), dtype=torch.int32, device=dev)
+    _native.call("cals_nnls_rows", rows, r, md.data_ptr(), r, hd.data_ptr(), ad.data_ptr(),
+                 xd.data_ptr(), r, cd.data_ptr(), int(max_iter),
+                 torch.cuda.current_stream().cuda_stream)
+    x = xd[:rows].cpu().numpy()
+    newbits = ad.cpu().numpy().view(np.uint32)[:rows]
+    act = ((newbits[:, None] >> np.arange(r, dtype=np.uint32)) & 1).astype(bool)
+    return x, act, cd.cpu().numpy()[:rows].astype(bool)
 
 
-def nnls_update(*args, **kwargs):
-    raise NotImplementedError(_NEXT)
+def nnls_solve_row(h: np.ndarray, f: np.ndarray, active: np.ndarray | None = None,
+                   max_iter: int | None = None):
+    """min x^T h x - 2 f^T x s.t. x >= 0, warm-started (als.py:185-263);
+    returns (x, active, converged)."""
+    f = np.asarray(f, dtype=np.float64).ravel()
+    r = f.size
+    act = np.zeros((1, r), bool) if active is None else np.asarray(active, bool).reshape(1, r)
+    x, a, conv = _nnls_rows_gpu(f[None, :], h, act, -1 if max_iter is None else max_iter)
+    if not conv[0]:
+        warnings.warn("active-set search hit its iteration cap", NonConvergedNnlsWarning,
+                      stacklevel=2)
+    return x[0], a[0], bool(conv[0])
+
+
+def nnls_update(m: np.ndarray, h: np.ndarray, state: NnlsState, mode: int) -> np.ndarray:
+    """Row-wise non-negative update warm-started from ``state`` (als.py:266-278)."""
+    x, a, conv = _nnls_rows_gpu(np.asarray(m), h, state.active[mode], -1)
+    state.active[mode][...] = a
+    if not conv.all():
+        warnings.warn("active-set search hit its iteration cap", NonConvergedNnlsWarning,
+                      stacklevel=2)
+    return np.asfortranarray(x)
 
 
 def run_single_als(t, start, cfg: ConvergenceConfig, ls: LineSearchConfig | None = None,

@@ -1337,6 +1337,23 @@ int cals_engine_trace(cals_engine* e, int32_t* widths, int32_t* n_active, double
   return kOk;
 }
 
+int cals_engine_set_tensor(cals_engine* e, cals_tensor* t) {
+  CALS_CHECK(e && t, kErrInvalid, "null argument");
+  Engine* g = e->e;
+  CALS_CHECK(t->t->order == g->order, kErrInvalid, "tensor order differs from the engine's");
+  for (int n = 0; n < g->order; ++n)
+    CALS_CHECK(t->t->dims[n] == g->t->dims[n], kErrInvalid, "tensor dims differ from the engine's");
+  if (t->t != g->t) {
+    g->t = t->t;
+    // the captured graph embeds the old tensor's TMA descriptors
+    if (g->exec) cudaGraphExecDestroy(g->exec);
+    if (g->graph) cudaGraphDestroy(g->graph);
+    g->exec = nullptr;
+    g->graph = nullptr;
+  }
+  return kOk;
+}
+
 int cals_nnls_rows(int rows, int rank, const double* m, int64_t ldm, const double* h,
                    uint32_t* active, double* x, int64_t ldx, int32_t* converged, int max_iter,
                    void* stream) {

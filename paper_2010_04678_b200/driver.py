@@ -11,13 +11,15 @@ K=1 run reproduces that model's columns of a K>1 run exactly.
 from __future__ import annotations
 
 import enum
+import threading
 import time
+import warnings
 from dataclasses import dataclass, field
 from typing import Iterable
 
 import numpy as np
 
-from .als import ConvergenceConfig, LineSearchConfig, _NEXT
+from .als import ConvergenceConfig, LineSearchConfig, NonConvergedNnlsWarning
 from .engine import CalsEngine
 from .model import STATUS_FROM_CODE, Model, ModelStatus
 from .mttkrp import mttkrp_flops
@@ -70,17 +72,17 @@ def run(t: DenseTensor, models: Iterable[Model], cfg: ConvergenceConfig, *,
                 raise CapacityError(f"model {m.id!r} rank {m.rank} exceeds r_star {r_star}")
     if mode not in (ExecutionMode.SEQUENTIAL, ExecutionMode.PARALLEL, ExecutionMode.CALS):
         raise ValueError(f"unknown execution mode {mode!r}")
-    if nonneg:
-        raise NotImplementedError(_NEXT)
     if not queue:
         return []
     if t.sqnorm <= 0.0:
         raise ValueError("tensor squared norm must be positive")
     if mode is ExecutionMode.CALS:
-        return _run_fused(t, queue, cfg, r_star, trace, label_per_model=False, ls=ls)
+        return _run_fused(t, queue, cfg, r_star, trace, label_per_model=False, ls=ls,
+                          nonneg=nonneg)
     out = []
     for m in queue:
-        out += _run_fused(t, [m], cfg, m.rank, trace, label_per_model=True, ls=ls)
+        out += _run_fused(t, [m], cfg, m.rank, trace, label_per_model=True, ls=ls,
+                          nonneg=nonneg)
     return out
 
 
@@ -88,29 +90,82 @@ def _instance_flops(t: DenseTensor, rank: int, iterations: int) -> int:
     return iterations * t.order * mttkrp_flops(t.dims, rank)
 
 
+class _EngineCache:
+    """Device engines kept between ``run`` calls (keyed by shape, capacity and
+    the rank sequence) so repeated sweeps reuse every device allocation and
+    re-bind to the new tensor instead of re-allocating.  An engine is checked
+    out while in use, so concurrent callers never share one."""
+
+    def __init__(self, limit: int = 4):
+        self.limit = limit
+        self.free: list = []
+        self.lock = threading.Lock()
+
+    def acquire(self, dev, r_star: int, ranks, trace_capacity: int) -> CalsEngine:
+        key = (tuple(dev.dims), int(r_star), tuple(int(r) for r in ranks), int(trace_capacity))
+        with self.lock:
+            for i, (k, e) in enumerate(self.free):
+                if k == key:
+                    del self.free[i]
+                    e.set_tensor(dev)
+                    e._cache_key = key
+                    return e
+        e = CalsEngine(dev, r_star, ranks, trace_capacity=trace_capacity)
+        e._cache_key = key
+        return e
+
+    def release(self, e: CalsEngine) -> None:
+        with self.lock:
+            self.free.append((e._cache_key, e))
+            while len(self.free) > self.limit:
+                self.free.pop(0)[1].close()
+
+    def clear(self) -> None:
+        with self.lock:
+            for _, e in self.free:
+                e.close()
+            self.free.clear()
+
+
+_ENGINES = _EngineCache()
+
+
+def clear_engine_cache() -> None:
+    """Free the device workspaces kept between ``run`` calls."""
+    _ENGINES.clear()
+
+
 def _run_fused(t: DenseTensor, queue: list[Model], cfg: ConvergenceConfig, r_star: int,
                trace: list | None, label_per_model: bool,
-               ls: LineSearchConfig | None = None) -> list[Model]:
+               ls: LineSearchConfig | None = None, nonneg: bool = False) -> list[Model]:
     prof = LAST_RUN_PROFILE
     prof.clear()
     t0 = time.perf_counter()
     dev = t.device()
     t1 = time.perf_counter()
-    eng = CalsEngine(dev, r_star, [m.rank for m in queue],
-                     trace_capacity=_trace_cap(queue, cfg) if trace is not None else 1)
+    ranks = [m.rank for m in queue]
+    tcap = _trace_cap(queue, cfg) if trace is not None else 1
+    eng = _ENGINES.acquire(dev, r_star, ranks, tcap)
     t2 = time.perf_counter()
     try:
-        if ls is not None and ls.enabled:
-            eng.set_line_search(True, ls.alpha)
-        eng.load_pool(eng.pack([m.factors for m in queue]))
+        eng.set_line_search(bool(ls is not None and ls.enabled), None if ls is None else ls.alpha)
+        eng.set_nonneg(nonneg)
+        staging = eng.staging()
+        eng.load_pool(eng.pack([m.factors for m in queue], out=staging))
         tic = time.perf_counter()
         eng.run(cfg.tol, cfg.max_iterations, t.sqnorm)
         t4 = time.perf_counter()
-        res = eng.results()
+        res = eng.results(pool_out=staging)
+        warned = eng.nnls_warnings() if nonneg else None
         wall = time.perf_counter() - tic
         records = eng.trace() if (trace is not None and not label_per_model) else None
-    finally:
+    except BaseException:
         eng.close()
+        raise
+    _ENGINES.release(eng)
+    if warned is not None and warned.any():
+        warnings.warn("active-set search hit its iteration cap", NonConvergedNnlsWarning,
+                      stacklevel=3)
     t5 = time.perf_counter()
     prof.update(tensor_upload_s=t1 - t0, engine_create_s=t2 - t1, pool_upload_s=tic - t2,
                 device_loop_s=t4 - tic, results_download_s=t5 - t4)

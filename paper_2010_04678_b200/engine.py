@@ -67,9 +67,24 @@ class CalsEngine:
         assert at == self.pool_elems or (at == 0 and self.pool_elems == 0)
 
     # -------------------------------------------------------------- pool
-    def pack(self, factor_lists) -> np.ndarray:
+    def staging(self) -> np.ndarray:
+        """Page-locked host buffer of the pool's size (allocated once)."""
+        if getattr(self, "_staging", None) is None:
+            import torch
+
+            self._staging_t = torch.empty(max(self.pool_elems, 1), dtype=torch.float64,
+                                          pin_memory=True)
+            self._staging = self._staging_t.numpy()
+        return self._staging
+
+    def set_tensor(self, dev_tensor):
+        """Re-bind to another device tensor of the same shape."""
+        _native.call("cals_engine_set_tensor", self.handle, dev_tensor.handle)
+        self._tensor = dev_tensor
+
+    def pack(self, factor_lists, out: np.ndarray | None = None) -> np.ndarray:
         """Host pool: per model, per mode, row-major (I_n, R_k)."""
-        pool = np.empty(max(self.pool_elems, 1))
+        pool = np.empty(max(self.pool_elems, 1)) if out is None else out
         for k, facs in enumerate(factor_lists):
             r = int(self.ranks[k])
             for n_, f in enumerate(facs):
@@ -108,12 +123,15 @@ class CalsEngine:
                      float(sqnorm), 1 if use_graph else 0, s, C.byref(it))
         return it.value
 
-    def results(self, with_pool: bool = True, stream=None) -> EngineResults:
+    def results(self, with_pool: bool = True, stream=None, pool_out: np.ndarray | None = None
+                ) -> EngineResults:
         import torch
 
         s = stream if stream is not None else torch.cuda.current_stream().cuda_stream
         k = len(self.ranks)
-        pool = np.empty(max(self.pool_elems, 1)) if with_pool else None
+        pool = None
+        if with_pool:
+            pool = pool_out if pool_out is not None else np.empty(max(self.pool_elems, 1))
         status = np.empty(k, np.int32)
         iters = np.empty(k, np.int32)
         err = np.empty(k)
@@ -141,6 +159,15 @@ class CalsEngine:
         """Line search after every iteration (alpha None -> iteration^(1/3))."""
         _native.call("cals_engine_set_line_search", self.handle, 1 if enabled else 0,
                      0.0 if alpha is None else float(alpha))
+
+    def set_nonneg(self, enabled: bool):
+        """Non-negative (NNLS) factor updates, ranks <= 32."""
+        _native.call("cals_engine_set_nonneg", self.handle, 1 if enabled else 0)
+
+    def nnls_warnings(self) -> np.ndarray:
+        flags = np.zeros(max(len(self.ranks), 1), np.int32)
+        _native.call("cals_engine_nnls_warnings", self.handle, flags.ctypes.data)
+        return flags[:len(self.ranks)]
 
     # ------------------------------------------------------- step-wise
     def begin(self, tol: float, max_iterations: int, sqnorm: float, stream=None):
