@@ -12,8 +12,10 @@ sweep.
             last retirement; CUDA events on the launch stream, L2 flushed
             (256 MiB write) between steps, max over ranks.
   e2e    -- the public API ``paper_2010_04678_b200.run`` with host numpy
-            inputs: fresh DenseTensor each step (tensor H2D), pool H2D,
-            results D2H, Model objects built -- wall clock with device syncs.
+            inputs (tensor data in pinned host memory): a fresh DenseTensor
+            each step (tensor H2D), model pool H2D, results D2H and the Model
+            objects built -- wall clock with device syncs.  Device workspaces
+            persist between calls (the driver's engine cache).
   roofline -- the fused MTTKRP kernel (+ its split reduction) at the c2 shape
             and W=2100 through cals_mttkrp, CUDA events; algorithmic flops =
             2*W*prod(dims) per launch (mttkrp.py:72-76) against the FP64 DMMA
@@ -263,6 +265,7 @@ def main_gpu(args) -> None:
     # ---- e2e through the public API with host buffers
     from paper_2010_04678_b200.driver import LAST_RUN_PROFILE
 
+    t.pin()  # the step's host input lives in page-locked memory (contract: pinned host buffers)
     e2e_times, phases = [], []
     h2d = t.data.nbytes + pool_host.nbytes
     d2h = pool_host.nbytes + n_models * (4 * 3 + 8 * 3) + 8 * sum(m.rank for m in models)

@@ -652,6 +652,22 @@ struct Engine {
 
 static size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
 
+// Kernel attributes are process-global: several engines (different r_star,
+// ranks) share the kernels, so the dynamic shared-memory limit only ever
+// grows -- a cached engine must never find it lowered by a younger one.
+static cudaError_t raise_smem_limit(const void* func, size_t bytes) {
+  static std::mutex mu;
+  static std::map<const void*, size_t> cur;
+  std::lock_guard<std::mutex> lk(mu);
+  size_t& have = cur[func];
+  if (bytes <= have) return cudaSuccess;
+  const cudaError_t e =
+      cudaFuncSetAttribute(func, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+  if (e == cudaSuccess) have = bytes;
+  return e;
+}
+
+
 // Dimension tree for 3-way tensors (ALS order 0,1,2):
 //   Y-tree: Y = X x_3 A2 is shared by modes 0 and 1 (A2 is not updated
 //           between them); mode 2 is a full fused MTTKRP.
@@ -770,12 +786,8 @@ static int engine_create(Tensor* t, int capacity, int n_models, const int* ranks
     maxI = std::max(maxI, t->dims[n]);
   }
   e->move_grid = (int)std::max<long long>(1, std::min<long long>(rows_total, sms * 8));
-  CALS_CUDA_TRY(cudaFuncSetAttribute(e->upd_kernel,
-                                     cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     (int)e->upd_smem));
-  CALS_CUDA_TRY(cudaFuncSetAttribute(engine_move_kernel,
-                                     cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     (int)e->move_smem));
+  CALS_CUDA_TRY(raise_smem_limit((const void*)e->upd_kernel, e->upd_smem));
+  CALS_CUDA_TRY(raise_smem_limit((const void*)engine_move_kernel, e->move_smem));
 
   // arena layout
   struct Item { void** dst; size_t bytes; };
@@ -1009,9 +1021,7 @@ static int engine_set_nonneg(Engine* e, int enabled) {
                         size_t(kUpdThreads / 32) * kNnlsWs * 8;
     if (need > e->upd_smem) {
       e->upd_smem = need;
-      CALS_CUDA_TRY(cudaFuncSetAttribute(e->upd_kernel,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)e->upd_smem));
+      CALS_CUDA_TRY(raise_smem_limit((const void*)e->upd_kernel, e->upd_smem));
     }
   }
   if (h.nonneg != (enabled ? 1 : 0)) {
@@ -1049,9 +1059,7 @@ static int engine_set_line_search(Engine* e, int enabled, double alpha) {
       off += it.second;
     }
     e->ls_smem = size_t(kUpdThreads) * (kFastR + 1) * 8;
-    CALS_CUDA_TRY(cudaFuncSetAttribute(ls_candidate_kernel,
-                                       cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       (int)e->ls_smem));
+    CALS_CUDA_TRY(raise_smem_limit((const void*)ls_candidate_kernel, e->ls_smem));
   }
   if (h.ls_enabled != enabled || (enabled && h.ls_alpha != alpha)) {
     // the captured iteration graph depends on the line-search setting
@@ -1228,8 +1236,7 @@ int cals_update_factor(int rows, int rank, const double* m, int64_t ldm, const d
   CALS_CHECK(m && h && a && scratch && status, kErrInvalid, "null argument");
   const int nthr = pick_nthr(rank);
   const size_t smem = size_t(rank) * rank * 8 + size_t(rank) * nthr * 8;
-  CALS_CUDA_TRY(cudaFuncSetAttribute(standalone_update_kernel,
-                                     cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  CALS_CUDA_TRY(raise_smem_limit((const void*)standalone_update_kernel, smem));
   standalone_update_kernel<<<1, kUpdThreads, smem, (cudaStream_t)stream>>>(
       m, ldm, rows, rank, h, a, lda, scratch, nthr, status);
   CALS_CUDA_TRY(cudaGetLastError());
@@ -1363,8 +1370,7 @@ int cals_nnls_rows(int rows, int rank, const double* m, int64_t ldm, const doubl
   if (rows == 0) return kOk;
   const int warps = 4;
   const size_t smem = (size_t(rank) * rank + size_t(warps) * kNnlsWs) * 8;
-  CALS_CUDA_TRY(cudaFuncSetAttribute(nnls_rows_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     (int)smem));
+  CALS_CUDA_TRY(raise_smem_limit((const void*)nnls_rows_kernel, smem));
   const int blocks = std::max(1, std::min((rows + warps - 1) / warps, 148 * 8));
   nnls_rows_kernel<<<blocks, 32 * warps, smem, (cudaStream_t)stream>>>(
       rows, rank, m, ldm, h, active, x, ldx, converged, max_iter);

@@ -144,7 +144,12 @@ ModePlan make_plan(const Tensor& t, int mode) {
   }
   // q splits: a function of the shape only (never of the active width) so the
   // fused result of a column block is bitwise independent of its neighbours.
-  p.S = (int)std::min<long long>(p.Dq, 32);
+  static const int max_splits = [] {
+    const char* env = getenv("CALS_SPLITS");  // tuning knob; still shape-only
+    const int v = env ? atoi(env) : 0;
+    return v > 0 ? v : 32;
+  }();
+  p.S = (int)std::min<long long>(p.Dq, max_splits);
   if (p.S < 1) p.S = 1;
   return p;
 }

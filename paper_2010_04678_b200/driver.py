@@ -11,6 +11,7 @@ K=1 run reproduces that model's columns of a K>1 run exactly.
 from __future__ import annotations
 
 import enum
+import os
 import threading
 import time
 import warnings
@@ -102,7 +103,8 @@ class _EngineCache:
         self.lock = threading.Lock()
 
     def acquire(self, dev, r_star: int, ranks, trace_capacity: int) -> CalsEngine:
-        key = (tuple(dev.dims), int(r_star), tuple(int(r) for r in ranks), int(trace_capacity))
+        key = (tuple(dev.dims), int(r_star), tuple(int(r) for r in ranks), int(trace_capacity),
+               os.environ.get("CALS_TREE"), os.environ.get("CALS_SPLITS"))
         with self.lock:
             for i, (k, e) in enumerate(self.free):
                 if k == key:
