@@ -614,6 +614,7 @@ enum Tree : int { kTreeNone = 0, kTreeY = 1, kTreeZ = 2 };
 
 struct Engine {
   Tensor* t = nullptr;
+  unsigned long long tensor_uid = 0;
   int order = 0, n_models = 0, capacity = 0, max_slots = 0, max_rank = 0;
   long long ld = 0;
   std::vector<int> ranks;
@@ -733,6 +734,7 @@ static int engine_create(Tensor* t, int capacity, int n_models, const int* ranks
   CALS_CHECK(n_models >= 0, kErrInvalid, "n_models must be >= 0");
   std::unique_ptr<Engine> e(new Engine());
   e->t = t;
+  e->tensor_uid = t->uid;
   e->order = t->order;
   e->n_models = n_models;
   e->capacity = capacity;
@@ -1348,10 +1350,14 @@ int cals_engine_set_tensor(cals_engine* e, cals_tensor* t) {
   CALS_CHECK(e && t, kErrInvalid, "null argument");
   Engine* g = e->e;
   CALS_CHECK(t->t->order == g->order, kErrInvalid, "tensor order differs from the engine's");
+  // the previously bound tensor may already be destroyed: compare against the
+  // engine's own copy of the dims and the tensor's unique id, never the pointer
   for (int n = 0; n < g->order; ++n)
-    CALS_CHECK(t->t->dims[n] == g->t->dims[n], kErrInvalid, "tensor dims differ from the engine's");
-  if (t->t != g->t) {
+    CALS_CHECK(t->t->dims[n] == g->h_st.dims[n], kErrInvalid,
+               "tensor dims differ from the engine's");
+  if (t->t->uid != g->tensor_uid) {
     g->t = t->t;
+    g->tensor_uid = t->t->uid;
     // the captured graph embeds the old tensor's TMA descriptors
     if (g->exec) cudaGraphExecDestroy(g->exec);
     if (g->graph) cudaGraphDestroy(g->graph);

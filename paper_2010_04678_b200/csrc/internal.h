@@ -7,6 +7,7 @@
 
 #include <map>
 #include <mutex>
+#include <atomic>
 #include <memory>
 #include <string>
 #include <vector>
@@ -43,6 +44,7 @@ struct Tensor {
   double* data = nullptr;  // [i0p * prod(dims[1:])]
   bool owned = false;
   double sqnorm = -1.0;
+  unsigned long long uid = 0;  // unique per tensor_create (addresses get reused)
   std::vector<ModePlan> plans;
   // A-operand tensor maps cached per (mode, variant)
   std::map<std::pair<int, int>, CUtensorMap> amaps;

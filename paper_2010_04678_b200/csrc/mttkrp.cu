@@ -172,6 +172,8 @@ int tensor_create(int order, const int64_t* dims, const double* host, const doub
   CALS_CHECK((host != nullptr) != (dev != nullptr), kErrInvalid,
              "exactly one of host / device data must be given");
   std::unique_ptr<Tensor> t(new Tensor());
+  static std::atomic<unsigned long long> next_uid{1};
+  t->uid = next_uid.fetch_add(1);
   CALS_CUDA_TRY(cudaGetDevice(&t->device));
   t->order = order;
   long long rest = 1;

@@ -164,7 +164,6 @@ def _run_fused(t: DenseTensor, queue: list[Model], cfg: ConvergenceConfig, r_sta
     except BaseException:
         eng.close()
         raise
-    _ENGINES.release(eng)
     if warned is not None and warned.any():
         warnings.warn("active-set search hit its iteration cap", NonConvergedNnlsWarning,
                       stacklevel=3)
@@ -185,6 +184,7 @@ def _run_fused(t: DenseTensor, queue: list[Model], cfg: ConvergenceConfig, r_sta
                          error=float(res.error[k]), fit=float(res.fit[k]),
                          iterations_done=int(res.iterations[k]), status=status,
                          seconds_active=float(res.seconds_active[k]), meta=meta))
+    _ENGINES.release(eng)  # only now: res.pool is the engine's staging buffer
     prof["build_models_s"] = time.perf_counter() - t5
     if trace is not None:
         if label_per_model:

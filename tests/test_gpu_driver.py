@@ -116,6 +116,25 @@ def test_inputs_not_mutated_and_capacity(cals):
                  r_star=2)
 
 
+def test_engine_cache_rebinds_fresh_tensors(cals):
+    """Repeated run() calls reuse cached device engines; each call may bring a
+    new tensor (possibly allocated where a freed one lived) -- results must be
+    bitwise identical every time."""
+    base = cals.generate_synthetic((30, 26, 22), 4, 0.1, seed=4)
+    models = cals.build_models(base.dims, [1, 3, 5], 2, seed=2)
+    cfg = cals.ConvergenceConfig(tol=0.0, max_iterations=4)
+    first = None
+    for _ in range(4):
+        t = cals.DenseTensor(base.dims, base.data)
+        out = cals.run(t, models, cfg, r_star=18)
+        t.release_device()
+        fac = [f for m in out for f in m.factors]
+        if first is None:
+            first = fac
+        else:
+            assert all(np.array_equal(a, b) for a, b in zip(first, fac))
+
+
 def test_update_factor_golden(cals):
     g = np.load(os.path.join(GOLDEN, "update.npz"))
     for i in range(int(g["n_cases"])):
