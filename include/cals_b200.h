@@ -78,10 +78,12 @@ size_t cals_update_scratch_bytes(int rank);
 /* ---- device-resident CALS driver (replaces driver.py:185-307 `_run_cals`)
  * ranks[k] for the queued models in FIFO order; r_star = column capacity
  * (multimatrix.py:19, 123-167).  The starting factors live in the engine's
- * pool: per model k, per mode n, a row-major I_n x ranks[k] block, models
- * in queue order, modes ascending (cals_engine_pool gives the device
- * pointer; cals_engine_load_pool copies from host or device).  Results are
- * written back into the same pool. */
+ * pool: per model k, per mode n, a COLUMN-major I_n x ranks[k] block (the
+ * reference's Fortran factor, model.py:26-39, byte for byte), models in
+ * queue order, modes ascending (cals_engine_pool gives the device pointer;
+ * cals_engine_load_pool copies from host or device).  Results are written
+ * back into the same pool; the engine transposes to its row-major
+ * multi-matrices only at admission / retirement. */
 int cals_engine_create(cals_tensor* t, int r_star, int n_models, const int32_t* ranks,
                        int trace_capacity, cals_engine** out);
 int cals_engine_destroy(cals_engine* e);

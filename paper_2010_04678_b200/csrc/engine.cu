@@ -555,7 +555,7 @@ __global__ void engine_move_kernel(EngState* st) {
       const int r = e - st->mv_pre[lo];
       const int k = st->mv_model[lo];
       const int R = st->rank[k];
-      const long long po = st->pool_off[(long long)k * N + n] + i * R + r;
+      const long long po = st->pool_off[(long long)k * N + n] + r * st->dims[n] + i;
       if (snap && st->mv_kind[lo] != kMoveKeep) continue;
       switch (st->mv_kind[lo]) {
         case kMoveKeep: F[st->mv_dst[lo] + r] = row[st->mv_src[lo] + r]; break;
@@ -594,7 +594,8 @@ __global__ void lambdas_kernel(const EngState* st, const long long* lam_off, dou
       for (int n = 0; n < N; ++n) {
         const double* P = st->pool + st->pool_off[(long long)k * N + n];
         double s = 0.0;
-        for (long long i = 0; i < st->dims[n]; ++i) s = fma(P[i * R + r], P[i * R + r], s);
+        const double* col = P + r * st->dims[n];
+        for (long long i = 0; i < st->dims[n]; ++i) s = fma(col[i], col[i], s);
         prod *= sqrt(s);
       }
       lam[lam_off[k] + r] = prod;

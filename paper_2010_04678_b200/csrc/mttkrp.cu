@@ -190,7 +190,17 @@ int tensor_create(int order, const int64_t* dims, const double* host, const doub
     t->data = const_cast<double*>(dev);  // borrowed
   } else {
     const size_t bytes = size_t(t->i0p) * size_t(rest) * 8;
-    CALS_CUDA_TRY(cudaMalloc(&t->data, bytes));
+    // stream-ordered pool allocation: repeated sweeps over fresh tensors of
+    // the same shape reuse the pool's pages instead of cudaMalloc / cudaFree
+    static std::once_flag pool_once;
+    std::call_once(pool_once, [dev = t->device] {
+      cudaMemPool_t pool;
+      if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+        uint64_t keep = ~0ull;
+        cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+      }
+    });
+    CALS_CUDA_TRY(cudaMallocAsync(&t->data, bytes, stream));
     t->owned = true;
     if (host) {
       CALS_CUDA_TRY(cudaMemcpy2DAsync(t->data, t->i0p * 8, host, dims[0] * 8, dims[0] * 8,
@@ -212,7 +222,7 @@ int tensor_create(int order, const int64_t* dims, const double* host, const doub
 
 void tensor_destroy(Tensor* t) {
   if (!t) return;
-  if (t->owned && t->data) cudaFree(t->data);
+  if (t->owned && t->data) cudaFreeAsync(t->data, 0);
   delete t;
 }
 

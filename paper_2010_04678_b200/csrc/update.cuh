@@ -296,7 +296,9 @@ struct FastPairs {
 // Upper Cholesky of H (smem, R <= 32) by warp 0, lane b owning column b;
 // row k of U is broadcast with shuffles.  U overwrites the upper triangle;
 // inv_diag[k] = 1/U[k][k].  Fails like dpotrf (pivot <= 0 or NaN).
-__device__ inline void warp_cholesky_fast_nosync(double* H, int R, double* inv_diag, int* flag) {
+__device__ inline void warp_cholesky_fast_nosync(double* __restrict__ H, int R,
+                                                 double* __restrict__ inv_diag, int* flag) {
+  __shared__ double urow[32];  // row k of U, broadcast to the trailing update
   {
     const int lane = threadIdx.x;
     bool ok = true;
@@ -310,12 +312,15 @@ __device__ inline void warp_cholesky_fast_nosync(double* H, int R, double* inv_d
       double ukb = 0.0;
       if (lane == k) ukb = u;
       else if (lane > k && lane < R) ukb = H[k * R + lane] / u;
+      if (lane < R) urow[lane] = ukb;
       __syncwarp();
       if (lane >= k && lane < R) H[k * R + lane] = ukb;
       if (lane == k) inv_diag[k] = 1.0 / u;
-      for (int a = k + 1; a < R; ++a) {
-        const double uka = __shfl_sync(0xffffffffu, ukb, a);
-        if (lane >= a && lane < R) H[a * R + lane] = fma(-uka, ukb, H[a * R + lane]);
+      // column `lane` of the trailing matrix: independent RMWs (no aliasing
+      // with urow), so the loads pipeline
+      if (lane > k && lane < R) {
+#pragma unroll 4
+        for (int a = k + 1; a <= lane; ++a) H[a * R + lane] = fma(-urow[a], ukb, H[a * R + lane]);
       }
       __syncwarp();
     }
@@ -351,9 +356,11 @@ __device__ inline void block_gram_fast(const double* F, long long ld, int rows, 
 // Solve every row of the block against U (smem) / inv_diag, write A,
 // refresh G = A^T A and (want_inner) return sum(A o M).  Returns false when
 // a solution entry is non-finite (caller -> pinv path).
-__device__ inline bool block_solve_gram_fast(const double* U, const double* inv_diag, int R,
-                                             const double* Mb, long long ldm, int rows, double* A,
-                                             long long lda, double* Xs, double* G,
+__device__ inline bool block_solve_gram_fast(const double* __restrict__ U,
+                                             const double* __restrict__ inv_diag, int R,
+                                             const double* __restrict__ Mb, long long ldm,
+                                             int rows, double* __restrict__ A, long long lda,
+                                             double* __restrict__ Xs, double* __restrict__ G,
                                              bool want_inner, double* inner, double* red,
                                              bool first_chunk_staged = false) {
   const int P = fast_pitch(R);

@@ -172,6 +172,9 @@ def _run_fused(t: DenseTensor, queue: list[Model], cfg: ConvergenceConfig, r_sta
                 device_loop_s=t4 - tic, results_download_s=t5 - t4)
     for m in queue:
         m.status = ModelStatus.ACTIVE
+    # one copy out of the engine's pinned staging buffer; every returned
+    # factor is a Fortran view into this fresh array (the models own it)
+    owned = np.array(res.pool[:eng.pool_elems])
     order = np.argsort(res.retire_seq, kind="stable")
     lam_off = np.concatenate([[0], np.cumsum([m.rank for m in queue])])
     out = []
@@ -180,7 +183,7 @@ def _run_fused(t: DenseTensor, queue: list[Model], cfg: ConvergenceConfig, r_sta
         status = STATUS_FROM_CODE[int(res.status[k])]
         meta = dict(src.meta)
         meta["lambdas"] = res.lambdas[lam_off[k]:lam_off[k + 1]].copy()
-        out.append(Model(id=src.id, rank=src.rank, factors=eng.unpack(res.pool, k),
+        out.append(Model(id=src.id, rank=src.rank, factors=eng.unpack(owned, k),
                          error=float(res.error[k]), fit=float(res.fit[k]),
                          iterations_done=int(res.iterations[k]), status=status,
                          seconds_active=float(res.seconds_active[k]), meta=meta))

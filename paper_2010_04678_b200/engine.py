@@ -83,21 +83,22 @@ class CalsEngine:
         self._tensor = dev_tensor
 
     def pack(self, factor_lists, out: np.ndarray | None = None) -> np.ndarray:
-        """Host pool: per model, per mode, row-major (I_n, R_k)."""
+        """Host pool: per model, per mode, the Fortran (I_n, R_k) factor's
+        bytes (column-major) -- one concatenation, no per-element work."""
         pool = np.empty(max(self.pool_elems, 1)) if out is None else out
-        for k, facs in enumerate(factor_lists):
-            r = int(self.ranks[k])
-            for n_, f in enumerate(facs):
-                o = self.offsets[k, n_]
-                pool[o:o + self.dims[n_] * r] = np.ascontiguousarray(f, dtype=np.float64).ravel()
+        parts = [np.asarray(f, dtype=np.float64).ravel(order="F")
+                 for facs in factor_lists for f in facs]
+        if parts:
+            np.concatenate(parts, out=pool[:self.pool_elems])
         return pool[:self.pool_elems]
 
     def unpack(self, pool: np.ndarray, k: int) -> list[np.ndarray]:
+        """Fortran (I_n, R_k) views of model k's blocks in ``pool`` (no copy)."""
         r = int(self.ranks[k])
         out = []
         for n_ in range(self.order):
             o = self.offsets[k, n_]
-            out.append(np.asfortranarray(pool[o:o + self.dims[n_] * r].reshape(self.dims[n_], r)))
+            out.append(pool[o:o + self.dims[n_] * r].reshape((self.dims[n_], r), order="F"))
         return out
 
     def load_pool(self, pool, stream=None):
