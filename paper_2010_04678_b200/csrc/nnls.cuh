@@ -23,6 +23,7 @@ __device__ inline double nnls_solve_passive(const double* H, int R, unsigned P, 
   const int lane = threadIdx.x & 31;
   const int p = __popc(P);
   if (p == 0) return 0.0;
+  __syncwarp();  // the previous solve's lanes are done reading A / b
   double* A = Ws;                    // [p][kNnlsP]
   double* b = Ws + kNnlsP * 32;      // [32]
   const bool in = lane < R && ((P >> lane) & 1u);

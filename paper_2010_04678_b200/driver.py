@@ -75,7 +75,7 @@ def run(t: DenseTensor, models: Iterable[Model], cfg: ConvergenceConfig, *,
         raise ValueError(f"unknown execution mode {mode!r}")
     if not queue:
         return []
-    if t.sqnorm <= 0.0:
+    if t.device_sqnorm() <= 0.0:
         raise ValueError("tensor squared norm must be positive")
     if mode is ExecutionMode.CALS:
         return _run_fused(t, queue, cfg, r_star, trace, label_per_model=False, ls=ls,
@@ -155,7 +155,7 @@ def _run_fused(t: DenseTensor, queue: list[Model], cfg: ConvergenceConfig, r_sta
         staging = eng.staging()
         eng.load_pool(eng.pack([m.factors for m in queue], out=staging))
         tic = time.perf_counter()
-        eng.run(cfg.tol, cfg.max_iterations, t.sqnorm)
+        eng.run(cfg.tol, cfg.max_iterations, t.device_sqnorm())
         t4 = time.perf_counter()
         res = eng.results(pool_out=staging)
         warned = eng.nnls_warnings() if nonneg else None
@@ -183,7 +183,7 @@ def _run_fused(t: DenseTensor, queue: list[Model], cfg: ConvergenceConfig, r_sta
         status = STATUS_FROM_CODE[int(res.status[k])]
         meta = dict(src.meta)
         meta["lambdas"] = res.lambdas[lam_off[k]:lam_off[k + 1]].copy()
-        out.append(Model(id=src.id, rank=src.rank, factors=eng.unpack(owned, k),
+        out.append(Model._from_engine(id=src.id, rank=src.rank, factors=eng.unpack(owned, k),
                          error=float(res.error[k]), fit=float(res.fit[k]),
                          iterations_done=int(res.iterations[k]), status=status,
                          seconds_active=float(res.seconds_active[k]), meta=meta))

@@ -19,5 +19,5 @@ print("workload ok")
 PY
 for tool in memcheck racecheck synccheck; do
   echo "== $tool"
-  CALS_TREE=1 compute-sanitizer --tool $tool --print-limit 20 python /tmp/san_work.py 2>&1 | tail -4
+  CALS_TREE=1 compute-sanitizer --tool $tool --print-limit 20 python /tmp/san_work.py 2>&1 | tail -30
 done
