@@ -130,7 +130,7 @@ __device__ inline void decide_model(EngState* st, int k, double e) {
 // RB > 0: fast path (every rank <= RB, rows in registers, chunked Gram);
 // RB == 0: generic path for ranks up to 128.  Same reference semantics.
 template <int RB>
-__global__ void __launch_bounds__(kUpdThreads) engine_update_kernel(EngState* st, int n,
+__global__ void __launch_bounds__(kUpdThreads, 2) engine_update_kernel(EngState* st, int n,
                                                                      int nthr) {
   extern __shared__ __align__(16) double dsm[];
   __shared__ int flag;
@@ -201,14 +201,12 @@ __global__ void __launch_bounds__(kUpdThreads) engine_update_kernel(EngState* st
           warp_cholesky_fast_nosync(H, R, inv_diag, &flag);
         } else {
           const int P = fast_pitch(R);
-          for (int i = threadIdx.x - 32; i < rows; i += blockDim.x - 32) {
-            const double* mrow = Mb + (long long)i * ld;
-            for (int a = 0; a < R; ++a) {
-              const double v = mrow[a];
-              bad |= !isfinite(v);
-              if (i < kUpdThreads) X[i * P + a] = v;
-            }
-          }
+          const int nt = blockDim.x - 32;
+          const int c0 = min(rows, kUpdThreads);
+          bad |= stage_block(Mb, ld, c0, R, P, X, threadIdx.x - 32, nt);
+          if (rows > c0)
+            bad |= stage_block(Mb + (long long)c0 * ld, ld, rows - c0, R, P, nullptr,
+                               threadIdx.x - 32, nt);
         }
       } else {
         for (int i = threadIdx.x; i < rows; i += blockDim.x) {

@@ -203,9 +203,11 @@ int tensor_create(int order, const int64_t* dims, const double* host, const doub
     CALS_CUDA_TRY(cudaMallocAsync(&t->data, bytes, stream));
     t->owned = true;
     if (host) {
-      CALS_CUDA_TRY(cudaMemcpy2DAsync(t->data, t->i0p * 8, host, dims[0] * 8, dims[0] * 8,
-                                      rest, cudaMemcpyHostToDevice, stream));
-      if (t->i0p != dims[0]) {
+      if (t->i0p == dims[0]) {  // one linear DMA (full PCIe rate from pinned memory)
+        CALS_CUDA_TRY(cudaMemcpyAsync(t->data, host, bytes, cudaMemcpyHostToDevice, stream));
+      } else {
+        CALS_CUDA_TRY(cudaMemcpy2DAsync(t->data, t->i0p * 8, host, dims[0] * 8, dims[0] * 8,
+                                        rest, cudaMemcpyHostToDevice, stream));
         // zero the pad column (one double per row)
         CALS_CUDA_TRY(cudaMemset2DAsync(t->data + dims[0], t->i0p * 8, 0, 8, rest, stream));
       }

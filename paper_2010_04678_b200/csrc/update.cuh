@@ -334,6 +334,34 @@ __device__ inline bool warp_cholesky_fast(double* H, int R, double* inv_diag, in
   return *flag != 0;
 }
 
+// Copy rows [0, cnt) of the R-wide column block at Mb (row stride ld) into
+// Xs (pitch P; Xs == nullptr: check only).  Consecutive threads take
+// consecutive elements of the block, so a warp's loads cover a few rows'
+// contiguous R-double segments (coalesced) and four loads per thread are in
+// flight at once.  Returns nonzero when any value is non-finite.
+__device__ __forceinline__ int stage_block(const double* __restrict__ Mb, long long ld, int cnt, int R,
+                                  int P, double* __restrict__ Xs, int t0, int nt) {
+  int bad = 0;
+  const int total = cnt * R;
+  for (int e0 = t0; e0 < total; e0 += 4 * nt) {
+    double v[4];
+    int ii[4], aa[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int e = e0 + u * nt;
+      ii[u] = e / R;
+      aa[u] = e - ii[u] * R;
+      v[u] = e < total ? Mb[(long long)ii[u] * ld + aa[u]] : 0.0;
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      bad |= !isfinite(v[u]);
+      if (Xs != nullptr && e0 + u * nt < total) Xs[ii[u] * P + aa[u]] = v[u];
+    }
+  }
+  return bad;
+}
+
 // Gram of an existing column block (rows x R at F + off), chunked through Xs.
 __device__ inline void block_gram_fast(const double* F, long long ld, int rows, int R, double* Xs,
                                        double* G) {
@@ -341,13 +369,10 @@ __device__ inline void block_gram_fast(const double* F, long long ld, int rows, 
   FastPairs pr;
   pr.init(R);
   for (int base = 0; base < rows; base += kUpdThreads) {
-    const int i = base + threadIdx.x;
-    if (i < rows) {
-      const double* row = F + (long long)i * ld;
-      for (int a = 0; a < R; ++a) Xs[threadIdx.x * P + a] = row[a];
-    }
+    const int cnt = min(kUpdThreads, rows - base);
+    stage_block(F + (long long)base * ld, ld, cnt, R, P, Xs, threadIdx.x, kUpdThreads);
     __syncthreads();
-    pr.accumulate(Xs, P, min(kUpdThreads, rows - base));
+    pr.accumulate(Xs, P, cnt);
     __syncthreads();
   }
   pr.store(G, R);
@@ -355,8 +380,10 @@ __device__ inline void block_gram_fast(const double* F, long long ld, int rows, 
 
 // Solve every row of the block against U (smem) / inv_diag, write A,
 // refresh G = A^T A and (want_inner) return sum(A o M).  Returns false when
-// a solution entry is non-finite (caller -> pinv path).
-__device__ inline bool block_solve_gram_fast(const double* __restrict__ U,
+// a solution entry is non-finite (caller -> pinv path).  Rows go through Xs
+// in chunks of kUpdThreads: coalesced stage -> one thread per row solves in
+// place -> coalesced write-back (+ inner product against M) -> Gram pairs.
+__device__ __forceinline__ bool block_solve_gram_fast(const double* __restrict__ U,
                                              const double* __restrict__ inv_diag, int R,
                                              const double* __restrict__ Mb, long long ldm,
                                              int rows, double* __restrict__ A, long long lda,
@@ -369,12 +396,14 @@ __device__ inline bool block_solve_gram_fast(const double* __restrict__ U,
   double dot = 0.0;
   int bad = 0;
   for (int base = 0; base < rows; base += kUpdThreads) {
-    const int i = base + threadIdx.x;
-    if (i < rows) {
-      const double* m = Mb + (long long)i * ldm;
+    const int cnt = min(kUpdThreads, rows - base);
+    const double* Mc = Mb + (long long)base * ldm;
+    if (base > 0 || !first_chunk_staged) {
+      stage_block(Mc, ldm, cnt, R, P, Xs, threadIdx.x, kUpdThreads);
+      __syncthreads();
+    }
+    if (threadIdx.x < cnt) {
       double* x = Xs + threadIdx.x * P;
-      if (base > 0 || !first_chunk_staged)
-        for (int a = 0; a < R; ++a) x[a] = m[a];
       for (int k = 0; k < R; ++k) {  // U^T y = m
         const double xk = x[k] * inv_diag[k];
         x[k] = xk;
@@ -388,16 +417,18 @@ __device__ inline bool block_solve_gram_fast(const double* __restrict__ U,
 #pragma unroll 4
         for (int a = 0; a < k; ++a) x[a] = fma(-U[a * R + k], xk, x[a]);
       }
-      double* o = A + (long long)i * lda;
-      for (int a = 0; a < R; ++a) {
-        const double v = x[a];
-        bad |= !isfinite(v);
-        o[a] = v;
-        if (want_inner) dot = fma(v, m[a], dot);
-      }
     }
     __syncthreads();
-    pr.accumulate(Xs, P, min(kUpdThreads, rows - base));
+    double* Ac = A + (long long)base * lda;
+    const int total = cnt * R;
+    for (int e = threadIdx.x; e < total; e += kUpdThreads) {
+      const int i = e / R, a = e - i * R;
+      const double v = Xs[i * P + a];
+      bad |= !isfinite(v);
+      Ac[(long long)i * lda + a] = v;
+      if (want_inner) dot = fma(v, Mc[(long long)i * ldm + a], dot);
+    }
+    pr.accumulate(Xs, P, cnt);
     __syncthreads();
   }
   if (__syncthreads_or(bad)) return false;

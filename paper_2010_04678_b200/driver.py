@@ -75,7 +75,9 @@ def run(t: DenseTensor, models: Iterable[Model], cfg: ConvergenceConfig, *,
         raise ValueError(f"unknown execution mode {mode!r}")
     if not queue:
         return []
-    if t.device_sqnorm() <= 0.0:
+    # (the ||T||^2 > 0 check runs in _run_fused, on the device copy, once
+    # the uploads are queued -- still before any model is touched)
+    if t._sqnorm is not None and t._sqnorm <= 0.0:
         raise ValueError("tensor squared norm must be positive")
     if mode is ExecutionMode.CALS:
         return _run_fused(t, queue, cfg, r_star, trace, label_per_model=False, ls=ls,
@@ -140,10 +142,12 @@ def clear_engine_cache() -> None:
 def _run_fused(t: DenseTensor, queue: list[Model], cfg: ConvergenceConfig, r_star: int,
                trace: list | None, label_per_model: bool,
                ls: LineSearchConfig | None = None, nonneg: bool = False) -> list[Model]:
+    import torch
+
     prof = LAST_RUN_PROFILE
     prof.clear()
     t0 = time.perf_counter()
-    dev = t.device()
+    dev = t.device()  # queued: the tensor upload overlaps the host packing below
     t1 = time.perf_counter()
     ranks = [m.rank for m in queue]
     tcap = _trace_cap(queue, cfg) if trace is not None else 1
@@ -152,42 +156,52 @@ def _run_fused(t: DenseTensor, queue: list[Model], cfg: ConvergenceConfig, r_sta
     try:
         eng.set_line_search(bool(ls is not None and ls.enabled), None if ls is None else ls.alpha)
         eng.set_nonneg(nonneg)
-        staging = eng.staging()
-        eng.load_pool(eng.pack([m.factors for m in queue], out=staging))
+        eng.load_pool(eng.pack([m.factors for m in queue], out=eng.staging()))
+        t3 = time.perf_counter()
+        sqnorm = t.device_sqnorm()  # waits for both uploads
+        if sqnorm <= 0.0:
+            raise _BadNorm()
         tic = time.perf_counter()
-        eng.run(cfg.tol, cfg.max_iterations, t.device_sqnorm())
+        eng.run(cfg.tol, cfg.max_iterations, sqnorm)
         t4 = time.perf_counter()
-        res = eng.results(pool_out=staging)
+        # the result pool lands in a fresh page-locked block (torch's caching
+        # host allocator -> no cudaHostAlloc per run) that the returned
+        # factors view directly: no host-side copy
+        pool_t = torch.empty(max(eng.pool_elems, 1), dtype=torch.float64, pin_memory=True)
+        res = eng.results(pool_out=pool_t.numpy())
         warned = eng.nnls_warnings() if nonneg else None
         wall = time.perf_counter() - tic
         records = eng.trace() if (trace is not None and not label_per_model) else None
+    except _BadNorm:
+        _ENGINES.release(eng)  # nothing ran: the engine stays reusable
+        raise ValueError("tensor squared norm must be positive") from None
     except BaseException:
         eng.close()
         raise
+    _ENGINES.release(eng)
     if warned is not None and warned.any():
         warnings.warn("active-set search hit its iteration cap", NonConvergedNnlsWarning,
                       stacklevel=3)
     t5 = time.perf_counter()
-    prof.update(tensor_upload_s=t1 - t0, engine_create_s=t2 - t1, pool_upload_s=tic - t2,
-                device_loop_s=t4 - tic, results_download_s=t5 - t4)
+    prof.update(tensor_upload_s=t1 - t0, engine_create_s=t2 - t1, pool_upload_s=t3 - t2,
+                upload_wait_s=tic - t3, device_loop_s=t4 - tic, results_download_s=t5 - t4)
     for m in queue:
         m.status = ModelStatus.ACTIVE
-    # one copy out of the engine's pinned staging buffer; every returned
-    # factor is a Fortran view into this fresh array (the models own it)
-    owned = np.array(res.pool[:eng.pool_elems])
-    order = np.argsort(res.retire_seq, kind="stable")
-    lam_off = np.concatenate([[0], np.cumsum([m.rank for m in queue])])
+    pool = res.pool
+    order = np.argsort(res.retire_seq, kind="stable").tolist()
+    lam_off = np.concatenate([[0], np.cumsum(ranks)]).tolist()
+    status, err, fit = res.status.tolist(), res.error.tolist(), res.fit.tolist()
+    iters, secs = res.iterations.tolist(), res.seconds_active.tolist()
+    lam = res.lambdas
     out = []
     for k in order:
         src = queue[k]
-        status = STATUS_FROM_CODE[int(res.status[k])]
         meta = dict(src.meta)
-        meta["lambdas"] = res.lambdas[lam_off[k]:lam_off[k + 1]].copy()
-        out.append(Model._from_engine(id=src.id, rank=src.rank, factors=eng.unpack(owned, k),
-                         error=float(res.error[k]), fit=float(res.fit[k]),
-                         iterations_done=int(res.iterations[k]), status=status,
-                         seconds_active=float(res.seconds_active[k]), meta=meta))
-    _ENGINES.release(eng)  # only now: res.pool is the engine's staging buffer
+        meta["lambdas"] = lam[lam_off[k]:lam_off[k + 1]]
+        out.append(Model._from_engine(id=src.id, rank=src.rank, factors=eng.unpack(pool, k),
+                                      error=err[k], fit=fit[k], iterations_done=iters[k],
+                                      status=STATUS_FROM_CODE[status[k]],
+                                      seconds_active=secs[k], meta=meta))
     prof["build_models_s"] = time.perf_counter() - t5
     if trace is not None:
         if label_per_model:
@@ -202,6 +216,10 @@ def _run_fused(t: DenseTensor, queue: list[Model], cfg: ConvergenceConfig, r_sta
                     label="cals-iteration", flops=t.order * mttkrp_flops(t.dims, width),
                     seconds=secs, meta={"width": width, "n_active": n_active}))
     return out
+
+
+class _BadNorm(Exception):
+    pass
 
 
 def _trace_cap(queue, cfg) -> int:

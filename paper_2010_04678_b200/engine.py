@@ -94,12 +94,11 @@ class CalsEngine:
 
     def unpack(self, pool: np.ndarray, k: int) -> list[np.ndarray]:
         """Fortran (I_n, R_k) views of model k's blocks in ``pool`` (no copy)."""
-        r = int(self.ranks[k])
-        out = []
-        for n_ in range(self.order):
-            o = self.offsets[k, n_]
-            out.append(pool[o:o + self.dims[n_] * r].reshape((self.dims[n_], r), order="F"))
-        return out
+        if getattr(self, "_blocks", None) is None:  # plain-int (offset, shape) per block
+            self._blocks = [[(int(self.offsets[j, n_]), int(self.dims[n_]) * int(r),
+                              (int(self.dims[n_]), int(r))) for n_ in range(self.order)]
+                            for j, r in enumerate(self.ranks)]
+        return [pool[o:o + size].reshape(shape, order="F") for o, size, shape in self._blocks[k]]
 
     def load_pool(self, pool, stream=None):
         """``pool`` is a host ndarray or a CUDA tensor (device-to-device copy)."""
@@ -107,9 +106,11 @@ class CalsEngine:
 
         s = stream if stream is not None else torch.cuda.current_stream().cuda_stream
         if isinstance(pool, np.ndarray):
+            # stream-ordered (async from pinned memory); ``run`` synchronises
+            # before returning, so the buffer may be reused after it
             pool = np.ascontiguousarray(pool, dtype=np.float64)
             _native.call("cals_engine_load_pool", self.handle, pool.ctypes.data, 0, s)
-            torch.cuda.current_stream().synchronize()
+            self._pool_src = pool
         else:
             _native.call("cals_engine_load_pool", self.handle, C.c_void_p(pool.data_ptr()), 1, s)
 
