@@ -668,6 +668,28 @@ static cudaError_t raise_smem_limit(const void* func, size_t bytes) {
 }
 
 
+// the tree contraction's split partials sit at the start of the engine
+// workspace, its Ozaki Lo slices after them
+static size_t tree_ws_offset(const ModePlan& p, long long ld) {
+  return align_up(size_t(p.S) * size_t(p.M) * size_t(ld) * 8, 256);
+}
+
+// Ozaki X slices for every view this engine contracts (built once per tensor,
+// before any graph capture).
+static int engine_prepare_slices(Engine* e, cudaStream_t stream) {
+  Tensor& t = *e->t;
+  const int N = e->order;
+  for (int n = 0; n < N; ++n) {
+    const bool used = e->tree == kTreeNone || n == N - 1 || (e->tree == kTreeZ && n == 0);
+    if (!used) continue;
+    const int rc = ozaki_prepare(t, t.plans[n], n, stream);
+    if (rc) return rc;
+  }
+  if (e->tree == kTreeY) return ozaki_prepare(t, e->tree_plan, 100, stream);
+  if (e->tree == kTreeZ) return ozaki_prepare(t, e->tree_plan, 1, stream);
+  return kOk;
+}
+
 // Dimension tree for 3-way tensors (ALS order 0,1,2):
 //   Y-tree: Y = X x_3 A2 is shared by modes 0 and 1 (A2 is not updated
 //           between them); mode 2 is a full fused MTTKRP.
@@ -703,7 +725,7 @@ static int setup_tree(Engine* e) {
   } else {
     p = t.plans[1];  // MIDDLE: slab product over q = k is Z[j, k, :]
   }
-  e->ws_bytes = std::max(e->ws_bytes, size_t(p.S) * size_t(p.M) * size_t(e->ld) * 8 + 256);
+  e->ws_bytes = std::max(e->ws_bytes, tree_ws_offset(p, e->ld) + ozaki_ws_bytes(p, e->ld) + 256);
   CALS_CUDA_TRY(cudaMalloc(&e->d_partial, bytes));
   e->tree_variant = choose_variant(p.M, e->capacity, p.S);
   e->tree = choice;
@@ -920,13 +942,20 @@ static int enqueue_mode_mttkrp(Engine* e, int n, cudaStream_t stream) {
   double* const* F = e->h_st.F;
   double* Mo = e->h_st.Mout;
   const long long ld = e->ld, cap = e->capacity;
+  void* oz_ws = nullptr;
+  size_t oz_bytes = 0;
+  if (e->tree != kTreeNone) {
+    oz_bytes = ozaki_ws_bytes(e->tree_plan, ld);
+    oz_ws = reinterpret_cast<char*>(e->d_ws) + tree_ws_offset(e->tree_plan, ld);
+  }
   {
     int rc = kOk;
     if (e->tree == kTreeY && n == 0) {
       // M0 = sum_j A1[j] (sum_k X[:,j,k] A2[k]); the inner slab products are
       // the partial Y[i + I0p j] kept for mode 1
       rc = launch_contraction(t, e->tree_plan, 100, F[2], t.dims[2], ld, F[1], ld, 0, wptr, cap,
-                              Mo, ld, e->d_ws, e->tree_variant, stream, e->d_partial, ld, t.i0p);
+                              Mo, ld, e->d_ws, e->tree_variant, stream, e->d_partial, ld, t.i0p,
+                              oz_ws, oz_bytes);
     } else if (e->tree == kTreeY && n == 1) {
       // M1 = Y x_i A0(new): A2 unchanged since Y was formed
       rc = launch_partial_ttv(e->d_partial, ld, t.i0p, t.dims[1], 0, t.dims[0], F[0], ld, 0,
@@ -934,7 +963,8 @@ static int enqueue_mode_mttkrp(Engine* e, int n, cudaStream_t stream) {
     } else if (e->tree == kTreeZ && n == 1) {
       // M1 = sum_k A2[k] (sum_i X[i,:,k] A0(new)[i]); slab products = Z[j + I1 k]
       rc = launch_contraction(t, e->tree_plan, 1, F[0], t.dims[0], ld, F[2], ld, 0, wptr, cap, Mo,
-                              ld, e->d_ws, e->tree_variant, stream, e->d_partial, ld, t.dims[1]);
+                              ld, e->d_ws, e->tree_variant, stream, e->d_partial, ld, t.dims[1],
+                              oz_ws, oz_bytes);
     } else if (e->tree == kTreeZ && n == 2) {
       // M2 = Z x_j A1(new): A0 unchanged since Z was formed
       rc = launch_partial_ttv(e->d_partial, ld, t.dims[1], t.dims[2], 0, t.dims[1], F[1], ld, 0,
@@ -1107,6 +1137,8 @@ static int engine_run(Engine* e, double tol, int max_iterations, double sqnorm, 
     if (iterations_out) *iterations_out = 0;
     return kOk;
   }
+  rc = engine_prepare_slices(e, stream);
+  if (rc) return rc;
   // initial admission
   engine_plan_kernel<<<1, 32, 0, stream>>>(e->d_st);
   engine_move_kernel<<<e->move_grid, 256, e->move_smem, stream>>>(e->d_st);
@@ -1424,6 +1456,8 @@ int cals_engine_begin(cals_engine* e, double tol, int max_iterations, double sqn
     *g->h_done = 1;
     return kOk;
   }
+  rc = engine_prepare_slices(g, s);
+  if (rc) return rc;
   return enqueue_plan(g, s);  // initial admission
 }
 

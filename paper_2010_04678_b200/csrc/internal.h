@@ -33,6 +33,14 @@ struct ModePlan {
   bool hi_ones() const { return hi_modes.empty(); }
 };
 
+// Ozaki slices of one tensor view (ozaki.cuh): xs[7][Dq][M][Kp] int8, rex[Dq][M].
+struct OzSlices {
+  uint8_t* xs = nullptr;
+  int* rex = nullptr;
+  long long Kp = 0, M = 0, Dq = 0, Dp = 0;
+  CUtensorMap map;
+};
+
 // Device-resident dense tensor, mode-0 fastest, I0 padded to even so every
 // 3-D view has 16-byte aligned TMA strides.  Zero padding contributes nothing.
 struct Tensor {
@@ -48,6 +56,8 @@ struct Tensor {
   std::vector<ModePlan> plans;
   // A-operand tensor maps cached per (mode, variant)
   std::map<std::pair<int, int>, CUtensorMap> amaps;
+  // Ozaki X slices per view key (mode index, or >= 100 for engine-private views)
+  std::map<int, OzSlices> oz;
   std::mutex mu;
 };
 
@@ -86,11 +96,28 @@ int launch_mttkrp(Tensor& t, int mode, const FactorSet& f, int width, const int*
 // with explicit Lo [lrows][lo_ld] / Hi [Dq][hi_ld] operands.  map_key caches
 // the tensor map (modes use their index, engine-private plans use >= 100).
 // S > 1 needs `part` (S * M * lo_ld doubles) and reduces into `out`.
+// With `oz_ws` (>= ozaki_ws_bytes) and prepared Ozaki slices for map_key the
+// contraction runs on the INT8 tensor cores (ozaki.cuh); otherwise on DMMA.
 int launch_contraction(Tensor& t, const ModePlan& p, int map_key, const double* lo,
                        long long lrows, long long lo_ld, const double* hi, long long hi_ld,
                        int width, const int* width_ptr, long long cap, double* out, long long ldo,
                        double* part, int variant, cudaStream_t stream, double* side = nullptr,
-                       long long side_ld = 0, long long side_qstride = 0);
+                       long long side_ld = 0, long long side_qstride = 0, void* oz_ws = nullptr,
+                       size_t oz_ws_bytes = 0);
+
+// Ozaki-sliced INT8 tensor-core contraction (ozaki.cu) ------------------------
+bool ozaki_enabled();                       // CALS_MTTKRP=dmma disables it
+bool ozaki_eligible(const ModePlan& p);
+size_t ozaki_ws_bytes(const ModePlan& p, long long cap);  // per-call Lo slices
+// Build (once per tensor and key) the X slices of view `p`; stream-ordered.
+int ozaki_prepare(Tensor& t, const ModePlan& p, int key, cudaStream_t stream);
+void ozaki_release(Tensor& t);
+int launch_contraction_ozaki(Tensor& t, const ModePlan& p, int key, const double* lo,
+                             long long lrows, long long lo_ld, const double* hi, long long hi_ld,
+                             int width, const int* width_ptr, long long cap, double* out,
+                             long long ldo, double* part, void* oz_ws, size_t oz_ws_bytes,
+                             cudaStream_t stream, double* side, long long side_ld,
+                             long long side_qstride);
 
 // out[row][c] = sum over the reduced index of P[a + Da*b][c] * F[idx][c]
 // (reduce_b: rows a < rows_out, sum b < Db with F[b]; else rows b, sum a < La
@@ -105,6 +132,9 @@ int encode_map_2d(CUtensorMap* m, const double* base, long long inner, long long
                   long long ld_elems, int box_inner, int box_outer);
 int encode_map_3d(CUtensorMap* m, const double* base, long long d0, long long d1, long long d2,
                   int b0, int b1, int b2);
+
+int encode_map_u8(CUtensorMap* m, const void* base, int rank, const uint64_t* dims,
+                  const uint64_t* strides_bytes, const uint32_t* box);  // SWIZZLE_32B
 
 int sm_count(int device);
 

@@ -77,6 +77,28 @@ int encode_map_3d(CUtensorMap* m, const double* base, long long d0, long long d1
   return kOk;
 }
 
+// uint8 K-major operand maps for the Ozaki kernel: 32-byte inner box with the
+// 32-byte swizzle the tcgen05 SWIZZLE_32B descriptors expect.
+int encode_map_u8(CUtensorMap* m, const void* base, int rank, const uint64_t* dims,
+                  const uint64_t* strides_bytes, const uint32_t* box) {
+  auto enc = get_encode();
+  CALS_CHECK(enc, kErrCuda, "cuTensorMapEncodeTiled unavailable");
+  cuuint64_t d[5], st[4];
+  cuuint32_t b[5], es[5];
+  for (int i = 0; i < rank; ++i) {
+    d[i] = dims[i];
+    b[i] = box[i];
+    es[i] = 1;
+    if (i + 1 < rank) st[i] = strides_bytes[i];
+  }
+  CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_UINT8, rank, const_cast<void*>(base), d, st, b, es,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_32B,
+                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  CALS_CHECK(r == CUDA_SUCCESS, kErrCuda,
+             "cuTensorMapEncodeTiled(u8) failed: code " + std::to_string((int)r));
+  return kOk;
+}
+
 // ------------------------------------------------------------------ tensor --
 __global__ void sqnorm_partial_kernel(const double* __restrict__ x, long long n,
                                       double* __restrict__ part) {
@@ -224,6 +246,7 @@ int tensor_create(int order, const int64_t* dims, const double* host, const doub
 
 void tensor_destroy(Tensor* t) {
   if (!t) return;
+  ozaki_release(*t);
   if (t->owned && t->data) cudaFreeAsync(t->data, 0);
   delete t;
 }
@@ -406,6 +429,7 @@ size_t mttkrp_workspace_bytes(const Tensor& t, int mode, long long cap) {
   if (p.S > 1) b += size_t(p.S) * size_t(p.M) * size_t(ld) * 8;
   if (!p.lo_direct()) b += size_t(p.Dp) * size_t(ld) * 8;
   if (!p.hi_direct()) b += size_t(std::max<long long>(p.Dq, 1)) * size_t(ld) * 8;
+  if (ozaki_eligible(p)) b += ozaki_ws_bytes(p, ld) + 256;
   return b + 256;
 }
 
@@ -472,15 +496,45 @@ int launch_mttkrp(Tensor& t, int mode, const FactorSet& f, int width, const int*
     CALS_CUDA_TRY(cudaGetLastError());
     hi = buf;
   }
+  // INT8 tensor-core path: X slices built once per tensor (never inside a
+  // graph capture -- the engine prepares them before capturing)
+  void* oz_ws = nullptr;
+  size_t oz_bytes = 0;
+  if (ozaki_eligible(p)) {
+    char* o = reinterpret_cast<char*>((reinterpret_cast<uintptr_t>(wsp) + 255) & ~uintptr_t(255));
+    const size_t need = ozaki_ws_bytes(p, f.ld);
+    if (o + need <= reinterpret_cast<char*>(workspace) + workspace_bytes) {
+      cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+      CALS_CUDA_TRY(cudaStreamIsCapturing(stream, &cs));
+      if (cs == cudaStreamCaptureStatusNone) {
+        const int rc = ozaki_prepare(t, p, mode, stream);
+        if (rc) return rc;
+      }
+      oz_ws = o;
+      oz_bytes = need;
+    }
+  }
   return launch_contraction(t, p, mode, lo, lrows, lo_ld, hi, hi_ld, width, width_ptr, cap, out,
-                            ldo, part, variant, stream);
+                            ldo, part, variant, stream, nullptr, 0, 0, oz_ws, oz_bytes);
 }
 
 int launch_contraction(Tensor& t, const ModePlan& p, int map_key, const double* lo,
                        long long lrows, long long lo_ld, const double* hi, long long hi_ld,
                        int width, const int* width_ptr, long long cap, double* out, long long ldo,
                        double* part, int variant, cudaStream_t stream, double* side,
-                       long long side_ld, long long side_qstride) {
+                       long long side_ld, long long side_qstride, void* oz_ws,
+                       size_t oz_ws_bytes) {
+  static const bool dbg = getenv("CALS_DEBUG_OZ") != nullptr;
+  if (dbg)
+    fprintf(stderr, "[oz] contraction key=%d role=%d M=%lld Dp=%lld Dq=%lld S=%d oz_ws=%p elig=%d\n",
+            map_key, p.role, p.M, p.Dp, p.Dq, p.S, oz_ws, (int)ozaki_eligible(p));
+  if (oz_ws && ozaki_eligible(p)) {
+    const int rc = launch_contraction_ozaki(t, p, map_key, lo, lrows, lo_ld, hi, hi_ld, width,
+                                            width_ptr, cap, out, ldo, part, oz_ws, oz_ws_bytes,
+                                            stream, side, side_ld, side_qstride);
+    if (dbg) fprintf(stderr, "[oz]   ozaki rc=%d\n", rc);
+    if (rc != kErrUnsupported) return rc;  // unsupported = slices not prepared: DMMA below
+  }
   if (variant < 0) variant = choose_variant(p.M, cap, p.S);
   const VariantEntry& ve = kVariants[variant];
   const int sms = sm_count(t.device);

@@ -1,0 +1,343 @@
+// Host side of the Ozaki-sliced INT8 tensor-core MTTKRP (see ozaki.cuh):
+// per-tensor X slices (built once per tensor view), per-call Lo slices, and
+// the launch that replaces the DMMA contraction of mttkrp.cu.
+#include <cstdlib>
+#include <cstring>
+
+#include "internal.h"
+#include "mttkrp.cuh"
+#include "ozaki.cuh"
+
+namespace cals {
+
+using namespace oz;
+
+// X slices of one 3-D view: xs[7][Dq][M][Kp] (int8 bit patterns), rex[Dq][M] =
+// scale exponent ex per row (q, m).  Element (m, p, q) lives at x[m*sm + p*sp + q*sq].
+// Block = 256 threads for rows m0..m0+31 of slab q; padded p in [Dp, Kp) -> 0.
+__global__ void oz_slice_rows_kernel(const double* __restrict__ x, long long sm, long long sp,
+                                     long long sq, int M, int Dp, int Kp, int Dq,
+                                     uint8_t* __restrict__ xs, int* __restrict__ rex) {
+  __shared__ double tile[32][33];
+  __shared__ double red[8][33];
+  __shared__ int ex[32];
+  const int q = blockIdx.y, m0 = blockIdx.x * 32;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const double* xq = x + (long long)q * sq;
+  const bool mfast = sm == 1;  // m contiguous in memory -> lanes along m
+  // ---- pass 1: per-row max |x|
+  if (mfast) {
+    const int m = m0 + lane;
+    double mx = 0.0;
+    if (m < M)
+      for (int p = w; p < Dp; p += 8) mx = fmax(mx, fabs(xq[m + (long long)p * sp]));
+    red[w][lane] = mx;
+    __syncthreads();
+    if (w == 0) {
+      double v = red[0][lane];
+#pragma unroll
+      for (int k = 1; k < 8; ++k) v = fmax(v, red[k][lane]);
+      red[0][lane] = v;
+    }
+  } else {
+    for (int r = w; r < 32; r += 8) {
+      const int m = m0 + r;
+      double v = 0.0;
+      if (m < M)
+        for (int p = lane; p < Dp; p += 32) v = fmax(v, fabs(xq[(long long)m * sm + (long long)p * sp]));
+#pragma unroll
+      for (int o = 16; o; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
+      if (lane == 0) red[0][r] = v;
+    }
+  }
+  __syncthreads();
+  if (w == 0) {
+    const int e = scale_exp(red[0][lane]);
+    ex[lane] = e;
+    const int m = m0 + lane;
+    if (m < M) rex[(long long)q * M + m] = e;
+  }
+  __syncthreads();
+  // ---- pass 2: slices, written p-contiguous (32-byte segments per warp store)
+  const size_t slice_stride = size_t(Dq) * size_t(M) * size_t(Kp);
+  for (int p0 = 0; p0 < Kp; p0 += 32) {
+    if (mfast) {
+      const int m = m0 + lane;
+      for (int pp = w; pp < 32; pp += 8) {
+        const int p = p0 + pp;
+        tile[lane][pp] = (m < M && p < Dp) ? xq[m + (long long)p * sp] : 0.0;
+      }
+    } else {
+      const int p = p0 + lane;
+      for (int r = w; r < 32; r += 8) {
+        const int m = m0 + r;
+        tile[r][lane] = (m < M && p < Dp) ? xq[(long long)m * sm + (long long)p * sp] : 0.0;
+      }
+    }
+    __syncthreads();
+    for (int r = w; r < 32; r += 8) {
+      const int m = m0 + r;
+      if (m >= M) continue;
+      uint8_t s[kSlices];
+      slice7(tile[r][lane], ex[r], s);
+      uint8_t* dst = xs + (size_t(q) * M + m) * size_t(Kp) + p0 + lane;
+#pragma unroll
+      for (int k = 0; k < kSlices; ++k) dst[k * slice_stride] = s[k];
+    }
+    __syncthreads();
+  }
+}
+
+// Lo slices: ls[7][cap_pad][Kp] (column c of lo as a p-contiguous row),
+// cex[c] = scale exponent el of column c.  Block = 256 threads for columns c0..c0+31.
+__global__ void oz_slice_cols_kernel(const double* __restrict__ lo, long long ld, int Dp, int Kp,
+                                     const int* width_ptr, int width, long long cap_pad,
+                                     uint8_t* __restrict__ ls, int* __restrict__ cex) {
+  __shared__ double tile[32][33];
+  __shared__ double red[8][33];
+  __shared__ int ex[32];
+  const int W = width_ptr ? *width_ptr : width;
+  const int c0 = blockIdx.x * 32;
+  if (c0 >= W) return;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  {
+    const int c = c0 + lane;
+    double mx = 0.0;
+    if (c < W)
+      for (int p = w; p < Dp; p += 8) mx = fmax(mx, fabs(lo[(long long)p * ld + c]));
+    red[w][lane] = mx;
+  }
+  __syncthreads();
+  if (w == 0) {
+    double v = red[0][lane];
+#pragma unroll
+    for (int k = 1; k < 8; ++k) v = fmax(v, red[k][lane]);
+    const int e = scale_exp(v);
+    ex[lane] = e;
+    if (c0 + lane < W) cex[c0 + lane] = e;
+  }
+  __syncthreads();
+  const size_t slice_stride = size_t(cap_pad) * size_t(Kp);
+  for (int p0 = 0; p0 < Kp; p0 += 32) {
+    {
+      const int c = c0 + lane;
+      for (int pp = w; pp < 32; pp += 8) {
+        const int p = p0 + pp;
+        tile[pp][lane] = (c < W && p < Dp) ? lo[(long long)p * ld + c] : 0.0;
+      }
+    }
+    __syncthreads();
+    for (int cc = w; cc < 32; cc += 8) {
+      uint8_t s[kSlices];
+      slice7(tile[lane][cc], ex[cc], s);
+      uint8_t* dst = ls + size_t(c0 + cc) * size_t(Kp) + p0 + lane;
+#pragma unroll
+      for (int k = 0; k < kSlices; ++k) dst[k * slice_stride] = s[k];
+    }
+    __syncthreads();
+  }
+}
+
+static int view_strides(const Tensor& t, const ModePlan& p, long long& sm, long long& sp,
+                        long long& sq) {
+  const long long s0 = 1, s1 = p.D[0], s2 = p.D[0] * p.D[1];
+  switch (p.role) {
+    case kRoleFirst: sm = s0; sp = s1; sq = s2; break;    // (m, p, q)
+    case kRoleFirstQP: sm = s0; sq = s1; sp = s2; break;  // (m, q, p)
+    case kRoleMiddle: sp = s0; sm = s1; sq = s2; break;   // (p, m, q)
+    case kRoleLast: sp = s0; sq = s1; sm = s2; break;     // (p, q, m)
+    default: return kErrInvalid;
+  }
+  (void)t;
+  return kOk;
+}
+
+static long long kp_of(long long Dp) { return (Dp + KSTEP - 1) / KSTEP * KSTEP; }
+
+bool ozaki_enabled() {
+  static const bool on = [] {
+    const char* env = getenv("CALS_MTTKRP");
+    return !(env && (strcmp(env, "dmma") == 0 || strcmp(env, "0") == 0));
+  }();
+  return on;
+}
+
+// The INT8 path pays off when the tensor-core work per slab (K = Dp) is large
+// against the per-slab epilogue and the 64-row m-tiles are well filled
+// (measured: 200^3 1.23x, 500^3 2.2x faster than DMMA; an EEM mode with
+// M = 21 output rows is faster on DMMA).  CALS_MTTKRP=ozaki forces it for
+// every eligible shape, CALS_MTTKRP=dmma disables it.
+bool ozaki_eligible(const ModePlan& p) {
+  if (!ozaki_enabled() || p.role < 0 || p.role > 3 || kp_of(p.Dp) > 2048 || p.M < 1 ||
+      p.Dq < 1 || p.Dq > 65535)
+    return false;
+  static const bool force = [] {
+    const char* env = getenv("CALS_MTTKRP");
+    return env && strcmp(env, "ozaki") == 0;
+  }();
+  if (force) return true;
+  const double m_fill = double(p.M) / double((p.M + BNM - 1) / BNM * BNM);
+  const double k_fill = double(p.Dp) / double(kp_of(p.Dp));
+  return p.Dp >= 128 && m_fill * k_fill >= 0.6;
+}
+
+size_t ozaki_ws_bytes(const ModePlan& p, long long cap) {
+  const long long cap_pad = (cap + BMC - 1) / BMC * BMC;
+  return size_t(kSlices) * size_t(cap_pad) * size_t(kp_of(p.Dp)) + size_t(cap_pad) * 8 + 1024;
+}
+
+int ozaki_prepare(Tensor& t, const ModePlan& p, int key, cudaStream_t stream) {
+  if (!ozaki_eligible(p)) return kOk;
+  {
+    std::lock_guard<std::mutex> lk(t.mu);
+    if (t.oz.count(key)) return kOk;
+  }
+  long long sm, sp, sq;
+  if (view_strides(t, p, sm, sp, sq)) return kOk;
+  OzSlices o{};
+  o.Kp = kp_of(p.Dp);
+  o.M = p.M;
+  o.Dq = p.Dq;
+  o.Dp = p.Dp;
+  const size_t xs_bytes = size_t(kSlices) * size_t(p.Dq) * size_t(p.M) * size_t(o.Kp);
+  {
+    // too large for a third of the device: this view stays on DMMA
+    static const size_t total = [] {
+      size_t f = 0, tot = 0;
+      return cudaMemGetInfo(&f, &tot) == cudaSuccess ? tot : size_t(0);
+    }();
+    if (xs_bytes > total / 3) return kOk;
+  }
+  CALS_CUDA_TRY(cudaMallocAsync(reinterpret_cast<void**>(&o.xs), xs_bytes, stream));
+  CALS_CUDA_TRY(cudaMallocAsync(reinterpret_cast<void**>(&o.rex), size_t(p.Dq) * p.M * 4, stream));
+  dim3 grid((unsigned)((p.M + 31) / 32), (unsigned)p.Dq);
+  oz_slice_rows_kernel<<<grid, 256, 0, stream>>>(t.data, sm, sp, sq, (int)p.M, (int)p.Dp,
+                                                 (int)o.Kp, (int)p.Dq, o.xs, o.rex);
+  CALS_CUDA_TRY(cudaGetLastError());
+  {
+    const uint64_t dims[4] = {(uint64_t)o.Kp, (uint64_t)p.M, (uint64_t)p.Dq, (uint64_t)kSlices};
+    const uint64_t strides[3] = {(uint64_t)o.Kp, (uint64_t)(p.M * o.Kp),
+                                 (uint64_t)(p.Dq * p.M * o.Kp)};
+    const uint32_t box[4] = {KSTEP, BNM, 1, kSlices};
+    int rc = encode_map_u8(&o.map, o.xs, 4, dims, strides, box);
+    if (rc) return rc;
+  }
+  std::lock_guard<std::mutex> lk(t.mu);
+  if (t.oz.count(key)) {  // another thread raced us: keep theirs
+    cudaFreeAsync(o.xs, stream);
+    cudaFreeAsync(o.rex, stream);
+    return kOk;
+  }
+  t.oz.emplace(key, o);
+  return kOk;
+}
+
+void ozaki_release(Tensor& t) {
+  for (auto& kv : t.oz) {
+    cudaFreeAsync(kv.second.xs, 0);
+    cudaFreeAsync(kv.second.rex, 0);
+  }
+  t.oz.clear();
+}
+
+int launch_contraction_ozaki(Tensor& t, const ModePlan& p, int key, const double* lo,
+                             long long lrows, long long lo_ld, const double* hi, long long hi_ld,
+                             int width, const int* width_ptr, long long cap, double* out,
+                             long long ldo, double* part, void* oz_ws, size_t oz_ws_bytes,
+                             cudaStream_t stream, double* side, long long side_ld,
+                             long long side_qstride) {
+  OzSlices o;
+  {
+    std::lock_guard<std::mutex> lk(t.mu);
+    auto it = t.oz.find(key);
+    if (it == t.oz.end()) return kErrUnsupported;
+    o = it->second;
+  }
+  CALS_CHECK(o.M == p.M && o.Dq == p.Dq && o.Dp == p.Dp, kErrInvalid, "Ozaki slices / plan mismatch");
+  CALS_CHECK(oz_ws && oz_ws_bytes >= ozaki_ws_bytes(p, cap), kErrInvalid,
+             "Ozaki workspace too small");
+  CALS_CHECK(p.S == 1 || part != nullptr, kErrInvalid, "split-K needs a partial buffer");
+  const long long cap_pad = (cap + BMC - 1) / BMC * BMC;
+  uint8_t* ls = reinterpret_cast<uint8_t*>(oz_ws);
+  int* cex = reinterpret_cast<int*>(
+      (reinterpret_cast<uintptr_t>(ls + size_t(kSlices) * cap_pad * o.Kp) + 255) & ~uintptr_t(255));
+  const int sms = sm_count(t.device);
+
+  oz_slice_cols_kernel<<<(unsigned)((cap + 31) / 32), 256, 0, stream>>>(
+      lo, lo_ld, (int)std::min<long long>(lrows, p.Dp), (int)o.Kp, width_ptr, width, cap_pad, ls,
+      cex);
+  CALS_CUDA_TRY(cudaGetLastError());
+
+  CUtensorMap mapL;
+  {
+    const uint64_t dims[3] = {(uint64_t)o.Kp, (uint64_t)cap_pad, (uint64_t)kSlices};
+    const uint64_t strides[2] = {(uint64_t)o.Kp, (uint64_t)(cap_pad * o.Kp)};
+    const uint32_t box[3] = {KSTEP, BMC, kSlices};
+    int rc = encode_map_u8(&mapL, ls, 3, dims, strides, box);
+    if (rc) return rc;
+  }
+  Args a{};
+  a.M = (int)p.M;
+  a.KS = (int)(o.Kp / KSTEP);
+  a.Dq = (int)p.Dq;
+  a.S = p.S;
+  a.width = width;
+  a.width_ptr = width_ptr;
+  a.hi = hi;
+  a.ldh = hi_ld;
+  a.rex = o.rex;
+  a.cex = cex;
+  a.out = p.S > 1 ? part : out;
+  a.ldo = p.S > 1 ? lo_ld : ldo;
+  a.part_stride = (long long)p.M * lo_ld;
+  a.side = side;
+  a.ld_side = side_ld;
+  a.side_qstride = side_qstride;
+  static const int dbg = getenv("CALS_OZ_DBG") ? atoi(getenv("CALS_OZ_DBG")) : 0;
+  a.dbg = dbg;
+  static unsigned long long* prof = nullptr;
+  if ((dbg & 8) && !prof) cudaMalloc(&prof, 148 * 12 * 8);
+  a.prof = prof;
+  if (dbg & 8) {
+    static int calls = 0;
+    if (calls++ > 0) {
+      unsigned long long h[148 * 12];
+      cudaMemcpy(h, prof, sizeof(h), cudaMemcpyDeviceToHost);
+      unsigned long long mx = 0, sf = 0, st = 0, ns = 0;
+      int wi = 0;
+      for (int i = 0; i < 148; ++i) {
+        if (h[i * 4] > mx) { mx = h[i * 4]; sf = h[i * 4 + 1]; st = h[i * 4 + 2]; ns = h[i * 4 + 3]; wi = i; }
+      }
+      for (int k = 0; k < 2; ++k) {
+        const unsigned long long* e = h + 148 * 4 + (wi * 2 + k) * 4;
+        fprintf(stderr, "[ozprof]   epilogue warp %d: total %llu, wait_tfull %llu, load+release %llu, final %llu\n",
+                k ? 5 : 2, e[0], e[1], e[2], e[3]);
+      }
+      fprintf(stderr, "[ozprof] slowest CTA: total %llu clk, wait_full %llu, wait_tempty %llu, slabs %llu\n",
+              mx, sf, st, ns);
+    }
+  }
+
+  static std::once_flag attr_once;
+  static cudaError_t attr_err = cudaSuccess;
+  std::call_once(attr_once, [] {
+    attr_err = cudaFuncSetAttribute(mttkrp_ozaki_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    (int)kSmemBytes);
+  });
+  CALS_CUDA_TRY(attr_err);
+  const long long units = ((cap + BMC - 1) / BMC) * ((p.M + BNM - 1) / BNM) * p.S;
+  dim3 grid((unsigned)std::max<long long>(1, std::min<long long>(units, sms)));
+  mttkrp_ozaki_kernel<<<grid, kThreads, kSmemBytes, stream>>>(o.map, mapL, a);
+  CALS_CUDA_TRY(cudaGetLastError());
+  if (p.S > 1) {
+    const long long pairs = p.M * ((cap + 1) / 2);
+    const int blocks =
+        (int)std::max<long long>(1, std::min<long long>(sms * 8, (pairs + 255) / 256));
+    split_reduce_kernel<<<blocks, 256, 0, stream>>>(part, a.part_stride, p.S, (int)p.M, lo_ld,
+                                                    width_ptr, width, out, ldo);
+    CALS_CUDA_TRY(cudaGetLastError());
+  }
+  return kOk;
+}
+
+}  // namespace cals
