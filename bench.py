@@ -16,10 +16,12 @@ sweep.
             each step (tensor H2D), model pool H2D, results D2H and the Model
             objects built -- wall clock with device syncs.  Device workspaces
             persist between calls (the driver's engine cache).
-  roofline -- the fused MTTKRP kernel (+ its split reduction) at the c2 shape
-            and W=2100 through cals_mttkrp, CUDA events; algorithmic flops =
-            2*W*prod(dims) per launch (mttkrp.py:72-76) against the FP64 DMMA
-            peak measured live by cals_fp64_peak_probe.
+  roofline -- the fused MTTKRP (+ Lo slicing + split reduction) at the c2
+            shape and W=2100 through cals_mttkrp, CUDA events.  On the INT8
+            tensor-core (Ozaki) path: executed INT8 ops against the INT8 peak
+            measured live by cals_int8_peak_probe, plus the FP64-equivalent
+            rate (2*W*prod(dims) per launch, mttkrp.py:72-76) against the live
+            DMMA peak (cals_fp64_peak_probe); on the DMMA path the latter only.
   cpu_baseline -- the reference package (baseline/_ref, unmodified) on the
             host cores: one CALS iteration of the same workload, extrapolated
             to the 5-iteration sweep.
@@ -293,10 +295,14 @@ def main_gpu(args) -> None:
         dist.all_reduce(tmax, op=dist.ReduceOp.MAX)
     ms_max = float(tmax.item())
     value = total_models / (ms_max * 1e-3)
-    # launches per step: per iteration N x (mttkrp, reduce, update) + plan + move;
-    # plus the lookahead no-op iterations and the initial plan/move
-    iters_launched = int(np.mean(iters_run)) + 3
-    gpu_launches = iters_launched * (3 * 3 + 2) + 2
+    # launches per step (matches the ncu launch list of tools/ncu_engine.py):
+    # per driver iteration, order 3 with the dimension tree: two tensor-core
+    # contractions (+ split reduce, + the per-call Lo slicing on the INT8
+    # path), one partial TTV, three updates, plan + move; initial plan + move
+    k2, o2 = C.c_int32(), C.c_double()
+    _native.call("cals_mttkrp_kernel_info", dev_t.handle, 2, r_star, C.byref(k2), C.byref(o2))
+    per_contraction = 2 + (1 if k2.value == 1 else 0)
+    gpu_launches = int(round(np.mean(iters_run))) * (2 * per_contraction + 1 + 3 + 2) + 2
 
     # ---- e2e through the public API with host buffers
     from paper_2010_04678_b200.driver import LAST_RUN_PROFILE
@@ -326,17 +332,23 @@ def main_gpu(args) -> None:
            "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
            "phases_ms": {k: 1e3 * float(np.mean([p[k] for p in phases])) for k in phases[0]}}
 
-    # ---- roofline of the fused MTTKRP kernel at W = 2100
+    # ---- roofline of the fused MTTKRP kernel at the workload's capacity width
     peak = C.c_double()
     _native.call("cals_fp64_peak_probe", s, C.byref(peak))
+    peak_i8 = C.c_double()
+    _native.call("cals_int8_peak_probe", s, C.byref(peak_i8))
     W = r_star
     fac = [torch.rand((d, W), dtype=torch.float64, device="cuda") for d in dims]
     ptrs = (C.c_void_p * 3)(*[f.data_ptr() for f in fac])
     out_t = torch.empty((max(dims), W), dtype=torch.float64, device="cuda")
-    per_mode = []
+    per_mode, kinds, tops = [], [], []
     for n in range(3):
         b = C.c_size_t()
         _native.call("cals_mttkrp_workspace_bytes", dev_t.handle, n, W, C.byref(b))
+        kind, ops = C.c_int32(), C.c_double()
+        _native.call("cals_mttkrp_kernel_info", dev_t.handle, n, W, C.byref(kind), C.byref(ops))
+        kinds.append(int(kind.value))
+        tops.append(float(ops.value))
         work = torch.empty(b.value // 8 + 1, dtype=torch.float64, device="cuda")
         args_ = (dev_t.handle, n, W, ptrs, W, out_t.data_ptr(), W, work.data_ptr(), b.value,
                  eng.variant(n)["variant"], s)
@@ -351,22 +363,39 @@ def main_gpu(args) -> None:
         torch.cuda.synchronize()
         per_mode.append(e0.elapsed_time(e1) / reps)
     flops = 2.0 * W * np.prod(dims)
-    ach = flops / (np.mean(per_mode) * 1e-3) / 1e12
+    fp64_eq = flops / (np.mean(per_mode) * 1e-3) / 1e12
+    int8 = all(k == 1 for k in kinds)
     traffic = None
-    prof = os.path.join(ROOT, "profiles", "r01_mttkrp_ncu.json")
+    prof = os.path.join(ROOT, "profiles", "r01_ozaki_ncu.json" if int8 else "r01_mttkrp_ncu.json")
     if os.path.exists(prof):
         try:
             traffic = json.load(open(prof)).get("dram_bytes_per_launch")
         except Exception:
             traffic = None
-    roofline = {"bound": "tensor", "achieved": ach, "peak": peak.value, "unit": "TFLOP/s",
-                "frac": ach / peak.value, "traffic": traffic,
-                "kernel": f"mttkrp_dmma_kernel + split_reduce (cals_mttkrp), W={W}, "
-                          f"{args.config} shape",
-                "ms_per_launch_by_mode": per_mode,
-                "peak_source": "cals_fp64_peak_probe: DMMA.8x8x4 all SMs, measured live "
-                               "(MEASURED_PEAKS.json has no FP64 entry)",
-                "flops_per_launch": flops}
+    if int8:
+        ach = float(np.mean([o / (t * 1e-3) / 1e12 for o, t in zip(tops, per_mode)]))
+        roofline = {"bound": "tensor", "achieved": ach, "peak": peak_i8.value, "unit": "TOPS",
+                    "frac": ach / peak_i8.value, "traffic": traffic,
+                    "kernel": f"mttkrp_ozaki_kernel (INT8 tcgen05, 7x7 Ozaki slices, 28 products) "
+                              f"+ Lo slicing + split reduce (cals_mttkrp), W={W}, {args.config}",
+                    "achieved_counts": "executed INT8 ops: 2 x 28 slice products x padded "
+                                       "M x W x K tiles per slab",
+                    "peak_source": "cals_int8_peak_probe: tcgen05.mma kind::i8 M128 N256 K32 on "
+                                   "all SMs, measured live (MEASURED_PEAKS.json has no INT8 entry)",
+                    "fp64_equivalent": {"tflops": fp64_eq, "dmma_peak_tflops": peak.value,
+                                        "frac_of_dmma_peak": fp64_eq / peak.value,
+                                        "flops_per_launch": flops,
+                                        "definition": "2*W*prod(dims) (mttkrp.py:72-76) / time"},
+                    "ms_per_launch_by_mode": per_mode}
+    else:
+        roofline = {"bound": "tensor", "achieved": fp64_eq, "peak": peak.value, "unit": "TFLOP/s",
+                    "frac": fp64_eq / peak.value, "traffic": traffic,
+                    "kernel": f"mttkrp_dmma_kernel + split_reduce (cals_mttkrp), W={W}, "
+                              f"{args.config} shape",
+                    "ms_per_launch_by_mode": per_mode,
+                    "peak_source": "cals_fp64_peak_probe: DMMA.8x8x4 all SMs, measured live "
+                                   "(MEASURED_PEAKS.json has no FP64 entry)",
+                    "flops_per_launch": flops}
 
     it_mean = float(np.mean(iters_run))
     cfg = {"workload": wl["desc"], "dims": list(dims), "models_total": total_models,

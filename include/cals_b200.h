@@ -64,6 +64,12 @@ int cals_mttkrp(cals_tensor* t, int mode, int width, const double* const* factor
                 double* out, int64_t ldo, double* workspace, size_t workspace_bytes, int variant,
                 void* stream);
 int cals_mttkrp_variants(int* count);
+/* Which kernel the MTTKRP of `mode` runs on at `width` (0 = FP64 DMMA,
+ * 1 = Ozaki-sliced INT8 tcgen05) and the tensor-core operations one launch
+ * executes on it (FP64 flops incl. tile padding, or INT8 ops incl. the 28
+ * slice products and padding) -- for roofline accounting. */
+int cals_mttkrp_kernel_info(cals_tensor* t, int mode, int64_t width, int32_t* kernel,
+                            double* tensor_ops);
 
 /* ---- factor update (replaces als.py:74-96 `update_factor`) -------------
  * a = m h^{-1} for one rows x rank block (row-major m, a; h rank x rank):
@@ -156,6 +162,10 @@ int cals_engine_buffers(cals_engine* e, double** mttkrp_out, double** grams, int
  * Live FP64 tensor-core peak (DMMA.8x8x4 on every SM, TFLOP/s): the
  * roofline denominator for the fused MTTKRP. */
 int cals_fp64_peak_probe(void* stream, double* tflops);
+
+/* Live INT8 tensor-core peak (tcgen05.mma kind::i8, M=128 N=256 K=32 on every
+ * SM, TOPS): the roofline denominator of the Ozaki-sliced INT8 MTTKRP. */
+int cals_int8_peak_probe(void* stream, double* tops);
 
 #ifdef __cplusplus
 }

@@ -35,6 +35,7 @@ SIGNATURES = {
     "cals_mttkrp": (C.c_int, [C.c_void_p, C.c_int, C.c_int, c_void_pp, C.c_int64, C.c_void_p,
                               C.c_int64, C.c_void_p, C.c_size_t, C.c_int, C.c_void_p]),
     "cals_mttkrp_variants": (C.c_int, [c_int_p]),
+    "cals_mttkrp_kernel_info": (C.c_int, [C.c_void_p, C.c_int, C.c_int64, c_int_p, c_dbl_p]),
     "cals_update_factor": (C.c_int, [C.c_int, C.c_int, C.c_void_p, C.c_int64, C.c_void_p,
                                      C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p,
                                      C.c_void_p]),
@@ -54,6 +55,7 @@ SIGNATURES = {
                                     c_int_p]),
     "cals_engine_variant": (C.c_int, [C.c_void_p, C.c_int, c_int_p, c_int_p, c_int_p, c_int_p]),
     "cals_fp64_peak_probe": (C.c_int, [C.c_void_p, c_dbl_p]),
+    "cals_int8_peak_probe": (C.c_int, [C.c_void_p, c_dbl_p]),
     "cals_engine_set_line_search": (C.c_int, [C.c_void_p, C.c_int, C.c_double]),
     "cals_engine_set_nonneg": (C.c_int, [C.c_void_p, C.c_int]),
     "cals_nnls_rows": (C.c_int, [C.c_int, C.c_int, C.c_void_p, C.c_int64, C.c_void_p,

@@ -1257,6 +1257,25 @@ int cals_mttkrp(cals_tensor* t, int mode, int width, const double* const* factor
                        workspace_bytes, variant, (cudaStream_t)stream);
 }
 
+int cals_mttkrp_kernel_info(cals_tensor* t, int mode, int64_t width, int32_t* kernel,
+                            double* tensor_ops) {
+  CALS_CHECK(t && kernel && tensor_ops, kErrInvalid, "null argument");
+  CALS_CHECK(mode >= 0 && mode < t->t->order, kErrInvalid, "mode out of range");
+  CALS_CHECK(width >= 1, kErrInvalid, "width must be >= 1");
+  const ModePlan& p = t->t->plans[mode];
+  if (ozaki_eligible(p)) {
+    *kernel = 1;
+    *tensor_ops = ozaki_tensor_ops(p, width);
+  } else {
+    *kernel = 0;
+    const VariantInfo& v = variant_info(choose_variant(p.M, width, p.S));
+    const double mp = double((p.M + v.BM - 1) / v.BM * v.BM);
+    const double wp = double((width + v.BN - 1) / v.BN * v.BN);
+    *tensor_ops = 2.0 * mp * wp * double((p.Dp + 3) / 4 * 4) * double(p.Dq);
+  }
+  return kOk;
+}
+
 int cals_mttkrp_variants(int* count) {
   CALS_CHECK(count, kErrInvalid, "null argument");
   *count = num_variants();

@@ -109,6 +109,7 @@ int launch_contraction(Tensor& t, const ModePlan& p, int map_key, const double* 
 bool ozaki_enabled();                       // CALS_MTTKRP=dmma disables it
 bool ozaki_eligible(const ModePlan& p);
 size_t ozaki_ws_bytes(const ModePlan& p, long long cap);  // per-call Lo slices
+double ozaki_tensor_ops(const ModePlan& p, long long width);  // INT8 ops per launch
 // Build (once per tensor and key) the X slices of view `p`; stream-ordered.
 int ozaki_prepare(Tensor& t, const ModePlan& p, int key, cudaStream_t stream);
 void ozaki_release(Tensor& t);

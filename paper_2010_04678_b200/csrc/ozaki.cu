@@ -178,7 +178,16 @@ bool ozaki_eligible(const ModePlan& p) {
   if (force) return true;
   const double m_fill = double(p.M) / double((p.M + BNM - 1) / BNM * BNM);
   const double k_fill = double(p.Dp) / double(kp_of(p.Dp));
-  return p.Dp >= 128 && m_fill * k_fill >= 0.6;
+  // >= 3 slabs per split: the per-unit pipeline fill and the per-slab
+  // epilogue must amortise over enough tensor-core work
+  return p.Dp >= 128 && m_fill * k_fill >= 0.6 && p.Dq >= 3LL * p.S;
+}
+
+// 28 slice products x 2 ops per MAC over the padded tiles the kernel runs
+double ozaki_tensor_ops(const ModePlan& p, long long width) {
+  const double mp = double((p.M + BNM - 1) / BNM * BNM);
+  const double wp = double((width + BMC - 1) / BMC * BMC);
+  return 2.0 * 28.0 * mp * wp * double(kp_of(p.Dp)) * double(p.Dq);
 }
 
 size_t ozaki_ws_bytes(const ModePlan& p, long long cap) {

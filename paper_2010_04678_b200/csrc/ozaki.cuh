@@ -40,6 +40,7 @@
 #pragma once
 
 #include "common.cuh"
+#include "tcgen05.cuh"
 
 namespace cals {
 namespace oz {
@@ -84,157 +85,29 @@ struct Args {
   unsigned long long* prof;  // dbg & 8: per-CTA {total, wait_full, wait_tempty} cycles
 };
 
-// ------------------------------------------------------------ PTX wrappers --
-__device__ __forceinline__ void tc_fence_after() {
-  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-}
-__device__ __forceinline__ void tc_fence_before() {
-  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-}
-__device__ __forceinline__ void tc_commit(uint64_t* bar) {
-  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
-                   smem_u32(bar))
-               : "memory");
-}
-__device__ __forceinline__ void mma_i8(uint32_t d, uint64_t a, uint64_t b, uint32_t idesc,
-                                       uint32_t acc) {
-  asm volatile(
-      "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
-      "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n}\n" ::"r"(d),
-      "l"(a), "l"(b), "r"(idesc), "r"(acc)
-      : "memory");
-}
-// one elected lane of a converged warp issues (the operands are warp-uniform)
-__device__ __forceinline__ void mma_i8_elect(uint32_t d, uint64_t a, uint64_t b, uint32_t idesc,
-                                             uint32_t acc) {
-  asm volatile(
-      "{\n.reg .pred p, e;\nsetp.ne.b32 p, %4, 0;\nelect.sync _|e, 0xffffffff;\n"
-      "@e tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n}\n" ::"r"(d),
-      "l"(a), "l"(b), "r"(idesc), "r"(acc)
-      : "memory");
-}
-__device__ __forceinline__ void tc_commit_elect(uint64_t* bar) {
-  asm volatile(
-      "{\n.reg .pred e;\nelect.sync _|e, 0xffffffff;\n"
-      "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n}\n" ::"r"(
-          smem_u32(bar))
-      : "memory");
-}
-// All 28 slice products of one K step (group-major, i + j = g + 2), issued
-// by one elected lane from a single asm block: the 14 operand descriptors
-// and 7 accumulator addresses are formed once per K step.  `first` = K step
-// 0 of a slab: the first product of every group overwrites its accumulator.
-__device__ __forceinline__ void issue_kstep(uint32_t tmem, uint64_t a0, uint64_t b0,
-                                            uint32_t first) {
-  asm volatile(
-      "{\n"
-      ".reg .pred e, pf, pt;\n"
-      ".reg .b64 a<8>, b<8>;\n"
-      ".reg .b32 d<8>, iss, isu, ius, iuu;\n"
-      "setp.eq.u32 pf, %3, 0;\n"
-      "setp.eq.u32 pt, %3, %3;\n"
-      "mov.b64 a1, %1;\n"
-      "mov.b64 b1, %2;\n"
-      "add.s64 a2, %1, 256;\n"
-      "add.s64 b2, %2, 128;\n"
-      "add.s64 a3, %1, 512;\n"
-      "add.s64 b3, %2, 256;\n"
-      "add.s64 a4, %1, 768;\n"
-      "add.s64 b4, %2, 384;\n"
-      "add.s64 a5, %1, 1024;\n"
-      "add.s64 b5, %2, 512;\n"
-      "add.s64 a6, %1, 1280;\n"
-      "add.s64 b6, %2, 640;\n"
-      "add.s64 a7, %1, 1536;\n"
-      "add.s64 b7, %2, 768;\n"
-      "mov.b32 d0, %0;\n"
-      "add.u32 d1, %0, 64;\n"
-      "add.u32 d2, %0, 128;\n"
-      "add.u32 d3, %0, 192;\n"
-      "add.u32 d4, %0, 256;\n"
-      "add.u32 d5, %0, 320;\n"
-      "add.u32 d6, %0, 384;\n"
-      "mov.b32 iss, 135267488;\n"
-      "mov.b32 isu, 135266464;\n"
-      "mov.b32 ius, 135267360;\n"
-      "mov.b32 iuu, 135266336;\n"
-      "elect.sync _|e, 0xffffffff;\n"
-      "@e tcgen05.mma.cta_group::1.kind::i8 [d0], a1, b1, iss, pf;\n"
-      "@e tcgen05.mma.cta_group::1.kind::i8 [d1], a1, b2, isu, pf;\n"
-      "@e tcgen05.mma.cta_group::1.kind::i8 [d1], a2, b1, ius, pt;\n"
-      "@e tcgen05.mma.cta_group::1.kind::i8 [d2], a1, b3, isu, pf;\n"
-      "@e tcgen05.mma.cta_group::1.kind::i8 [d2], a2, b2, iuu, pt;\n"
-      "@e tcgen05.mma.cta_group::1.kind::i8 [d2], a3, b1, ius, pt;\n"
-      "@e tcgen05.mma.cta_group::1.kind::i8 [d3], a1, b4, isu, pf;\n"
-      "@e tcgen05.mma.cta_group::1.kind::i8 [d3], a2, b3, iuu, pt;\n"
-      "@e tcgen05.mma.cta_group::1.kind::i8 [d3], a3, b2, iuu, pt;\n"
-      "@e tcgen05.mma.cta_group::1.kind::i8 [d3], a4, b1, ius, pt;\n"
-      "@e tcgen05.mma.cta_group::1.kind::i8 [d4], a1, b5, isu, pf;\n"
-      "@e tcgen05.mma.cta_group::1.kind::i8 [d4], a2, b4, iuu, pt;\n"
-      "@e tcgen05.mma.cta_group::1.kind::i8 [d4], a3, b3, iuu, pt;\n"
-      "@e tcgen05.mma.cta_group::1.kind::i8 [d4], a4, b2, iuu, pt;\n"
-      "@e tcgen05.mma.cta_group::1.kind::i8 [d4], a5, b1, ius, pt;\n"
-      "@e tcgen05.mma.cta_group::1.kind::i8 [d5], a1, b6, isu, pf;\n"
-      "@e tcgen05.mma.cta_group::1.kind::i8 [d5], a2, b5, iuu, pt;\n"
-      "@e tcgen05.mma.cta_group::1.kind::i8 [d5], a3, b4, iuu, pt;\n"
-      "@e tcgen05.mma.cta_group::1.kind::i8 [d5], a4, b3, iuu, pt;\n"
-      "@e tcgen05.mma.cta_group::1.kind::i8 [d5], a5, b2, iuu, pt;\n"
-      "@e tcgen05.mma.cta_group::1.kind::i8 [d5], a6, b1, ius, pt;\n"
-      "@e tcgen05.mma.cta_group::1.kind::i8 [d6], a1, b7, isu, pf;\n"
-      "@e tcgen05.mma.cta_group::1.kind::i8 [d6], a2, b6, iuu, pt;\n"
-      "@e tcgen05.mma.cta_group::1.kind::i8 [d6], a3, b5, iuu, pt;\n"
-      "@e tcgen05.mma.cta_group::1.kind::i8 [d6], a4, b4, iuu, pt;\n"
-      "@e tcgen05.mma.cta_group::1.kind::i8 [d6], a5, b3, iuu, pt;\n"
-      "@e tcgen05.mma.cta_group::1.kind::i8 [d6], a6, b2, iuu, pt;\n"
-      "@e tcgen05.mma.cta_group::1.kind::i8 [d6], a7, b1, ius, pt;\n"
-      "}\n" ::"r"(tmem),
-      "l"(a0), "l"(b0), "r"(first)
-      : "memory");
-}
-
-// K-major, SWIZZLE_32B shared-memory matrix descriptor: rows of 32 bytes,
-// 8-row groups 256 B apart (SBO), version 1 (sm_100), layout code 6.
-__device__ __forceinline__ uint64_t desc_sw32(uint32_t saddr) {
-  return (uint64_t)((saddr >> 4) & 0x3FFF) | ((uint64_t)1 << 16) | ((uint64_t)(256 >> 4) << 32) |
-         ((uint64_t)1 << 46) | ((uint64_t)6 << 61);
-}
+// ------------------------------------------------------------ instruction --
 // kind::i8 instruction descriptor: S32 accumulate, K-major A and B, M = 128, N = 64
 __host__ __device__ constexpr uint32_t idesc_i8(int a_signed, int b_signed) {
   return (2u << 4) | ((uint32_t)a_signed << 7) | ((uint32_t)b_signed << 10) |
          ((uint32_t)(BNM >> 3) << 17) | ((uint32_t)(BMC >> 4) << 24);
 }
-__device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&r)[32]) {
-  asm volatile(
-      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,"
-      "%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
-      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
-        "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]),
-        "=r"(r[14]), "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]),
-        "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]),
-        "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
-      : "r"(taddr));
-  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-}
-__device__ __forceinline__ void tma_load_4d(void* dst, const CUtensorMap* m, uint64_t* bar, int c0,
-                                            int c1, int c2, int c3) {
-  asm volatile(
-      "cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes"
-      " [%0], [%1, {%3, %4, %5, %6}], [%2];" ::"r"(smem_u32(dst)),
-      "l"(reinterpret_cast<uint64_t>(m)), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2), "r"(c3)
-      : "memory");
-}
-
 // ------------------------------------------------------------------ slicing --
-// v in (-2^e, 2^e): 7 slices, s1 signed, s2..s7 unsigned (exact, see header)
+// v in (-2^e, 2^e): 7 slices, s1 signed, s2..s7 unsigned (see header).
+// |v| < 2^(e-55) is below the last slice and becomes 0: for a tiny negative
+// v, floor would give s1 = -1 and r = 1 + t, which rounds to exactly 1.0
+// when |t| < 2^-53 (the one inexact step of the split) and would turn into
+// a -2^(e-7) error.  Above the flush threshold r < 1 - 2^-48 and every
+// slice stays in range; the clamp is a second guard.
 __device__ __forceinline__ void slice7(double v, int e, uint8_t (&s)[kSlices]) {
   double t = ldexp(v, 7 - e);
+  if (fabs(t) < 0x1p-48) t = 0.0;
   double f = floor(t);
   s[0] = (uint8_t)(int8_t)(int)f;
   double r = t - f;
 #pragma unroll
   for (int k = 1; k < kSlices; ++k) {
     t = r * 256.0;
-    f = floor(t);
+    f = fmin(floor(t), 255.0);
     s[k] = (uint8_t)(int)f;
     r = t - f;
   }
@@ -256,9 +129,10 @@ __device__ __forceinline__ void unit_decode(int u, int tn, int tm, int& tile_c, 
   s = t / tm;
 }
 
-// 2^e as a double from its exponent field (exact for |e| <= 1022)
+// 2^e as a double: exponent-field construction in the normal range, ldexp
+// (subnormal / zero / inf) outside it
 __device__ __forceinline__ double pow2(int e) {
-  e = e < -1022 ? -1022 : (e > 1023 ? 1023 : e);
+  if (e < -1022 || e > 1023) return ldexp(1.0, e);
   return __hiloint2double((e + 1023) << 20, 0);
 }
 
