@@ -17,7 +17,8 @@ using namespace oz;
 // Block = 256 threads for rows m0..m0+31 of slab q; padded p in [Dp, Kp) -> 0.
 __global__ void oz_slice_rows_kernel(const double* __restrict__ x, long long sm, long long sp,
                                      long long sq, int M, int Dp, int Kp, int Dq,
-                                     uint8_t* __restrict__ xs, int* __restrict__ rex) {
+                                     uint8_t* __restrict__ xs, int* __restrict__ rex,
+                                     int* __restrict__ out_of_range) {
   __shared__ double tile[32][33];
   __shared__ double red[8][33];
   __shared__ int ex[32];
@@ -55,7 +56,11 @@ __global__ void oz_slice_rows_kernel(const double* __restrict__ x, long long sm,
     const int e = scale_exp(red[0][lane]);
     ex[lane] = e;
     const int m = m0 + lane;
-    if (m < M) rex[(long long)q * M + m] = e;
+    if (m < M) {
+      rex[(long long)q * M + m] = e;
+      // the epilogue scales by exponent-field adds: keep |ex| <= 900
+      if (e < -900 || e > 900) atomicOr(out_of_range, 1);
+    }
   }
   __syncthreads();
   // ---- pass 2: slices, written p-contiguous (32-byte segments per warp store)
@@ -219,10 +224,23 @@ int ozaki_prepare(Tensor& t, const ModePlan& p, int key, cudaStream_t stream) {
   }
   CALS_CUDA_TRY(cudaMallocAsync(reinterpret_cast<void**>(&o.xs), xs_bytes, stream));
   CALS_CUDA_TRY(cudaMallocAsync(reinterpret_cast<void**>(&o.rex), size_t(p.Dq) * p.M * 4, stream));
+  int* flag = nullptr;
+  CALS_CUDA_TRY(cudaMallocAsync(reinterpret_cast<void**>(&flag), sizeof(int), stream));
+  CALS_CUDA_TRY(cudaMemsetAsync(flag, 0, sizeof(int), stream));
   dim3 grid((unsigned)((p.M + 31) / 32), (unsigned)p.Dq);
   oz_slice_rows_kernel<<<grid, 256, 0, stream>>>(t.data, sm, sp, sq, (int)p.M, (int)p.Dp,
-                                                 (int)o.Kp, (int)p.Dq, o.xs, o.rex);
+                                                 (int)o.Kp, (int)p.Dq, o.xs, o.rex, flag);
   CALS_CUDA_TRY(cudaGetLastError());
+  // once per tensor and view: a tensor with rows beyond 2^+-900 stays on DMMA
+  int h_flag = 0;
+  CALS_CUDA_TRY(cudaMemcpyAsync(&h_flag, flag, sizeof(int), cudaMemcpyDeviceToHost, stream));
+  CALS_CUDA_TRY(cudaStreamSynchronize(stream));
+  CALS_CUDA_TRY(cudaFreeAsync(flag, stream));
+  if (h_flag) {
+    cudaFreeAsync(o.xs, stream);
+    cudaFreeAsync(o.rex, stream);
+    return kOk;
+  }
   {
     const uint64_t dims[4] = {(uint64_t)o.Kp, (uint64_t)p.M, (uint64_t)p.Dq, (uint64_t)kSlices};
     const uint64_t strides[3] = {(uint64_t)o.Kp, (uint64_t)(p.M * o.Kp),

@@ -29,7 +29,7 @@
 // CTA tile: 128 Lo columns c (the MMA M dimension = TMEM lanes) x 64 tensor
 // rows m (MMA N); K steps of 32 p.  Warp 0 = TMA producer, warp 1 = MMA
 // issuer (one thread), warps 2..9 = epilogue (TMEM -> registers -> FP64).
-// TMEM: 7 groups x 64 columns = 448 of 512.  Each group's accumulator is
+// TMEM: 8 rotating buffers x 64 columns for the 7 groups.  Each group's accumulator is
 // committed to its own mbarrier as soon as its last product of the slab is
 // issued and released by the epilogue as soon as it has been read, so the
 // epilogue of slab q overlaps the tail of slab q and the head of slab q+1.
@@ -59,6 +59,11 @@ constexpr int kStageBytes = kLoStageBytes + kXStageBytes;
 constexpr int kEpiWarps = 8;
 constexpr int kThreads = 32 * (2 + kEpiWarps);
 constexpr int kTmemCols = 512;
+// 8 accumulator buffers of 64 columns rotate over the 7 groups: group g of
+// the s-th slab uses buffer (7 s + g) mod 8, so the next slab's group g
+// overwrites the buffer of this slab's group g - 1 (drained one group
+// earlier) -- one group of slack between the epilogue and the MMA warp.
+constexpr int kTmemBufs = 8;
 // cross-slab FP64 accumulator of the epilogue: [32 rows m][256 epilogue threads]
 constexpr size_t kAccBytes = size_t(32) * 32 * kEpiWarps * 8;
 constexpr size_t kSmemBytes =
@@ -129,6 +134,13 @@ __device__ __forceinline__ void unit_decode(int u, int tn, int tm, int& tile_c, 
   s = t / tm;
 }
 
+// v * 2^k for v = (double) of an integer (0 or |v| in [1, 2^62)) and an
+// exponent k keeping the result normal: integer add on the exponent field
+__device__ __forceinline__ double exp_add(double v, int k) {
+  const int hi = __double2hiint(v);
+  return (hi & 0x7ff00000) ? __hiloint2double(hi + (k << 20), __double2loint(v)) : 0.0;
+}
+
 // 2^e as a double: exponent-field construction in the normal range, ldexp
 // (subnormal / zero / inf) outside it
 __device__ __forceinline__ double pow2(int e) {
@@ -148,8 +160,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * kStageBytes + kAccBytes);
   uint64_t* empty = full + STAGES;
   uint64_t* tfull = empty + STAGES;
-  uint64_t* tempty = tfull + kGroups;
-  uint32_t* tmem_base_slot = reinterpret_cast<uint32_t*>(tempty + kGroups);
+  uint64_t* tempty = tfull + kTmemBufs;
+  uint32_t* tmem_base_slot = reinterpret_cast<uint32_t*>(tempty + kTmemBufs);
 
   if ((smem_u32(smem) & 1023u) != 0) __trap();
   const int W = args.width_ptr ? *args.width_ptr : args.width;
@@ -166,9 +178,9 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_init(&full[i], 1);
       mbar_init(&empty[i], 1);
     }
-    for (int g = 0; g < kGroups; ++g) {
-      mbar_init(&tfull[g], 1);
-      mbar_init(&tempty[g], kEpiWarps);
+    for (int b = 0; b < kTmemBufs; ++b) {
+      mbar_init(&tfull[b], 1);
+      mbar_init(&tempty[b], kEpiWarps);
     }
     fence_barrier_init();
   }
@@ -238,29 +250,35 @@ __global__ void __launch_bounds__(kThreads, 1)
           // descriptor start-address field counts 16-byte units
           const uint64_t a0 = sdesc + (uint64_t)((stage * kStageBytes) >> 4);
           const uint64_t b0 = a0 + (uint64_t)(kLoStageBytes >> 4);
+          // group g of this slab -> buffer (7 slab + g) mod 8, use (7 slab + g) / 8
+          const uint32_t L0 = 7u * slab;
           if (ks > 0 && ks < KS - 1) {
-            issue_kstep(tmem, a0, b0, 0u);
+            uint32_t d[7];
+#pragma unroll
+            for (int g = 0; g < kGroups; ++g) d[g] = tmem + ((L0 + g) & 7u) * BNM;
+            issue_kstep(d, a0, b0, 0u);
           } else {
 #pragma unroll
             for (int g = 0; g < kGroups; ++g) {
               const int sum = g + 2;
               const int i_lo = sum - kSlices > 1 ? sum - kSlices : 1;
               const int i_hi = sum - 1 < kSlices ? sum - 1 : kSlices;
+              const uint32_t buf = (L0 + g) & 7u, use = (L0 + g) >> 3;
               if (ks == 0) {
-                // the epilogue must have drained this group's previous slab
+                // the epilogue must have drained this buffer's previous use
                 long long t1 = clock64();
-                mbar_wait(&tempty[g], (slab & 1u) ^ 1u);
+                mbar_wait(&tempty[buf], (use & 1u) ^ 1u);
                 tc_fence_after();
                 w_tempty += clock64() - t1;
               }
 #pragma unroll
               for (int i = i_lo; i <= i_hi; ++i) {
                 const int j = sum - i;
-                mma_i8_elect(tmem + g * BNM, a0 + (uint64_t)(((i - 1) * kLoTileBytes) >> 4),
+                mma_i8_elect(tmem + buf * BNM, a0 + (uint64_t)(((i - 1) * kLoTileBytes) >> 4),
                              b0 + (uint64_t)(((j - 1) * kXTileBytes) >> 4),
                              idesc_i8(i == 1, j == 1), (ks > 0 || i != i_lo) ? 1u : 0u);
               }
-              if (ks == KS - 1) tc_commit_elect(&tfull[g]);
+              if (ks == KS - 1) tc_commit_elect(&tfull[buf]);
             }
           }
           tc_commit_elect(&empty[stage]);
@@ -299,7 +317,11 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int c = tc * BMC + quad * 32 + lane;
       const bool cval = c < W;
       const int mb = tmi * BNM + half * 32;
-      const double cscale = cval ? pow2(args.cex[c] - 50) : 0.0;
+      const int kside = cval ? args.cex[c] - 50 : 0;
+      const double cscale = cval ? pow2(kside) : 0.0;
+      // exponent-add fast path for the side output: |ex| <= 900 and the
+      // result exponent field e_P + ex + kside (e_P in [1023, 1085]) in range
+      const bool side_fast = __all_sync(0xffffffffu, kside >= -122 && kside <= 61);
       // this thread's accumulator column in shared memory (touched once per
       // slab; keeps the registers for the TMEM values)
       double* acc = acc_s + (threadIdx.x - 64);
@@ -309,18 +331,19 @@ __global__ void __launch_bounds__(kThreads, 1)
         const double hc = cval ? __ldg(args.hi + (long long)q * args.ldh + c) * cscale : 0.0;
         // row scales of this warp's 32 rows: one coalesced load, broadcast
         // by shuffles (its latency hides behind the group drain)
-        const double rs_lane =
-            mb + lane < args.M ? pow2(__ldg(args.rex + (long long)q * args.M + mb + lane)) : 0.0;
+        const int rex_lane =
+            mb + lane < args.M ? __ldg(args.rex + (long long)q * args.M + mb + lane) : 0;
         auto drain = [&](int g, uint32_t (&v)[32]) {
           const long long e0 = clock64();
-          mbar_wait(&tfull[g], slab & 1u);
+          const uint32_t L = 7u * slab + g, buf = L & 7u;
+          mbar_wait(&tfull[buf], (L >> 3) & 1u);
           tc_fence_after();
           const long long e1 = clock64();
           ew_wait += e1 - e0;
-          tmem_ld32(trow + g * BNM, v);
+          tmem_ld32(trow + buf * BNM, v);
           tc_fence_before();
           __syncwarp();
-          if (lane == 0) mbar_arrive(&tempty[g]);  // TMEM group free for the next slab
+          if (lane == 0) mbar_arrive(&tempty[buf]);  // TMEM buffer free for its next use
           ew_load += clock64() - e1;
         };
         uint32_t v[32];
@@ -342,14 +365,32 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
         for (int j = 0; j < 32; ++j) P[j] = (double)(Qv[j] + (long long)((int)v[j] >> 12));
         const long long e2 = clock64();
+        // Scaling by 2^ex (row) and 2^(ex + el - 50) (side output) is an
+        // exponent-field add on the integer pipe: P is the double of an
+        // integer (0, or |P| in [1, 2^62)), row exponents are confined to
+        // [-900, 900] (ozaki_prepare falls back to DMMA otherwise) and the
+        // column term is checked per warp.  One DFMA per element is left.
+        if (side_fast) {
 #pragma unroll
-        for (int j = 0; j < 32; ++j) {
-          const int m = mb + j;
-          const double y = P[j] * __shfl_sync(0xffffffffu, rs_lane, j);
-          if (args.side && cval && m < args.M)
-            __stcg(args.side + ((long long)m + args.side_qstride * q) * args.ld_side + c,
-                   y * cscale);
-          acc[j * 32 * kEpiWarps] = fma(y, hc, acc[j * 32 * kEpiWarps]);
+          for (int j = 0; j < 32; ++j) {
+            const int m = mb + j;
+            const int ex = __shfl_sync(0xffffffffu, rex_lane, j);
+            const double y = exp_add(P[j], ex);
+            if (args.side && cval && m < args.M)
+              __stcg(args.side + ((long long)m + args.side_qstride * q) * args.ld_side + c,
+                     exp_add(P[j], ex + kside));
+            acc[j * 32 * kEpiWarps] = fma(y, hc, acc[j * 32 * kEpiWarps]);
+          }
+        } else {
+#pragma unroll
+          for (int j = 0; j < 32; ++j) {
+            const int m = mb + j;
+            const double y = exp_add(P[j], __shfl_sync(0xffffffffu, rex_lane, j));
+            if (args.side && cval && m < args.M)
+              __stcg(args.side + ((long long)m + args.side_qstride * q) * args.ld_side + c,
+                     y * cscale);
+            acc[j * 32 * kEpiWarps] = fma(y, hc, acc[j * 32 * kEpiWarps]);
+          }
         }
         ew_final += clock64() - e2;
       }

@@ -47,13 +47,14 @@ __device__ __forceinline__ void tc_commit_elect(uint64_t* bar) {
 // by one elected lane from a single asm block: the 14 operand descriptors
 // and 7 accumulator addresses are formed once per K step.  `first` = K step
 // 0 of a slab: the first product of every group overwrites its accumulator.
-__device__ __forceinline__ void issue_kstep(uint32_t tmem, uint64_t a0, uint64_t b0,
+// d[g] = TMEM address of group g's accumulator this slab (rotating buffers).
+__device__ __forceinline__ void issue_kstep(const uint32_t (&d)[7], uint64_t a0, uint64_t b0,
                                             uint32_t first) {
   asm volatile(
       "{\n"
       ".reg .pred e, pf, pt;\n"
       ".reg .b64 a<8>, b<8>;\n"
-      ".reg .b32 d<8>, iss, isu, ius, iuu;\n"
+      ".reg .b32 iss, isu, ius, iuu;\n"
       "setp.eq.u32 pf, %3, 0;\n"
       "setp.eq.u32 pt, %3, %3;\n"
       "mov.b64 a1, %1;\n"
@@ -70,48 +71,42 @@ __device__ __forceinline__ void issue_kstep(uint32_t tmem, uint64_t a0, uint64_t
       "add.s64 b6, %2, 640;\n"
       "add.s64 a7, %1, 1536;\n"
       "add.s64 b7, %2, 768;\n"
-      "mov.b32 d0, %0;\n"
-      "add.u32 d1, %0, 64;\n"
-      "add.u32 d2, %0, 128;\n"
-      "add.u32 d3, %0, 192;\n"
-      "add.u32 d4, %0, 256;\n"
-      "add.u32 d5, %0, 320;\n"
-      "add.u32 d6, %0, 384;\n"
       "mov.b32 iss, 135267488;\n"
       "mov.b32 isu, 135266464;\n"
       "mov.b32 ius, 135267360;\n"
       "mov.b32 iuu, 135266336;\n"
       "elect.sync _|e, 0xffffffff;\n"
-      "@e tcgen05.mma.cta_group::1.kind::i8 [d0], a1, b1, iss, pf;\n"
-      "@e tcgen05.mma.cta_group::1.kind::i8 [d1], a1, b2, isu, pf;\n"
-      "@e tcgen05.mma.cta_group::1.kind::i8 [d1], a2, b1, ius, pt;\n"
-      "@e tcgen05.mma.cta_group::1.kind::i8 [d2], a1, b3, isu, pf;\n"
-      "@e tcgen05.mma.cta_group::1.kind::i8 [d2], a2, b2, iuu, pt;\n"
-      "@e tcgen05.mma.cta_group::1.kind::i8 [d2], a3, b1, ius, pt;\n"
-      "@e tcgen05.mma.cta_group::1.kind::i8 [d3], a1, b4, isu, pf;\n"
-      "@e tcgen05.mma.cta_group::1.kind::i8 [d3], a2, b3, iuu, pt;\n"
-      "@e tcgen05.mma.cta_group::1.kind::i8 [d3], a3, b2, iuu, pt;\n"
-      "@e tcgen05.mma.cta_group::1.kind::i8 [d3], a4, b1, ius, pt;\n"
-      "@e tcgen05.mma.cta_group::1.kind::i8 [d4], a1, b5, isu, pf;\n"
-      "@e tcgen05.mma.cta_group::1.kind::i8 [d4], a2, b4, iuu, pt;\n"
-      "@e tcgen05.mma.cta_group::1.kind::i8 [d4], a3, b3, iuu, pt;\n"
-      "@e tcgen05.mma.cta_group::1.kind::i8 [d4], a4, b2, iuu, pt;\n"
-      "@e tcgen05.mma.cta_group::1.kind::i8 [d4], a5, b1, ius, pt;\n"
-      "@e tcgen05.mma.cta_group::1.kind::i8 [d5], a1, b6, isu, pf;\n"
-      "@e tcgen05.mma.cta_group::1.kind::i8 [d5], a2, b5, iuu, pt;\n"
-      "@e tcgen05.mma.cta_group::1.kind::i8 [d5], a3, b4, iuu, pt;\n"
-      "@e tcgen05.mma.cta_group::1.kind::i8 [d5], a4, b3, iuu, pt;\n"
-      "@e tcgen05.mma.cta_group::1.kind::i8 [d5], a5, b2, iuu, pt;\n"
-      "@e tcgen05.mma.cta_group::1.kind::i8 [d5], a6, b1, ius, pt;\n"
-      "@e tcgen05.mma.cta_group::1.kind::i8 [d6], a1, b7, isu, pf;\n"
-      "@e tcgen05.mma.cta_group::1.kind::i8 [d6], a2, b6, iuu, pt;\n"
-      "@e tcgen05.mma.cta_group::1.kind::i8 [d6], a3, b5, iuu, pt;\n"
-      "@e tcgen05.mma.cta_group::1.kind::i8 [d6], a4, b4, iuu, pt;\n"
-      "@e tcgen05.mma.cta_group::1.kind::i8 [d6], a5, b3, iuu, pt;\n"
-      "@e tcgen05.mma.cta_group::1.kind::i8 [d6], a6, b2, iuu, pt;\n"
-      "@e tcgen05.mma.cta_group::1.kind::i8 [d6], a7, b1, ius, pt;\n"
-      "}\n" ::"r"(tmem),
-      "l"(a0), "l"(b0), "r"(first)
+      "@e tcgen05.mma.cta_group::1.kind::i8 [%0], a1, b1, iss, pf;\n"
+      "@e tcgen05.mma.cta_group::1.kind::i8 [%4], a1, b2, isu, pf;\n"
+      "@e tcgen05.mma.cta_group::1.kind::i8 [%4], a2, b1, ius, pt;\n"
+      "@e tcgen05.mma.cta_group::1.kind::i8 [%5], a1, b3, isu, pf;\n"
+      "@e tcgen05.mma.cta_group::1.kind::i8 [%5], a2, b2, iuu, pt;\n"
+      "@e tcgen05.mma.cta_group::1.kind::i8 [%5], a3, b1, ius, pt;\n"
+      "@e tcgen05.mma.cta_group::1.kind::i8 [%6], a1, b4, isu, pf;\n"
+      "@e tcgen05.mma.cta_group::1.kind::i8 [%6], a2, b3, iuu, pt;\n"
+      "@e tcgen05.mma.cta_group::1.kind::i8 [%6], a3, b2, iuu, pt;\n"
+      "@e tcgen05.mma.cta_group::1.kind::i8 [%6], a4, b1, ius, pt;\n"
+      "@e tcgen05.mma.cta_group::1.kind::i8 [%7], a1, b5, isu, pf;\n"
+      "@e tcgen05.mma.cta_group::1.kind::i8 [%7], a2, b4, iuu, pt;\n"
+      "@e tcgen05.mma.cta_group::1.kind::i8 [%7], a3, b3, iuu, pt;\n"
+      "@e tcgen05.mma.cta_group::1.kind::i8 [%7], a4, b2, iuu, pt;\n"
+      "@e tcgen05.mma.cta_group::1.kind::i8 [%7], a5, b1, ius, pt;\n"
+      "@e tcgen05.mma.cta_group::1.kind::i8 [%8], a1, b6, isu, pf;\n"
+      "@e tcgen05.mma.cta_group::1.kind::i8 [%8], a2, b5, iuu, pt;\n"
+      "@e tcgen05.mma.cta_group::1.kind::i8 [%8], a3, b4, iuu, pt;\n"
+      "@e tcgen05.mma.cta_group::1.kind::i8 [%8], a4, b3, iuu, pt;\n"
+      "@e tcgen05.mma.cta_group::1.kind::i8 [%8], a5, b2, iuu, pt;\n"
+      "@e tcgen05.mma.cta_group::1.kind::i8 [%8], a6, b1, ius, pt;\n"
+      "@e tcgen05.mma.cta_group::1.kind::i8 [%9], a1, b7, isu, pf;\n"
+      "@e tcgen05.mma.cta_group::1.kind::i8 [%9], a2, b6, iuu, pt;\n"
+      "@e tcgen05.mma.cta_group::1.kind::i8 [%9], a3, b5, iuu, pt;\n"
+      "@e tcgen05.mma.cta_group::1.kind::i8 [%9], a4, b4, iuu, pt;\n"
+      "@e tcgen05.mma.cta_group::1.kind::i8 [%9], a5, b3, iuu, pt;\n"
+      "@e tcgen05.mma.cta_group::1.kind::i8 [%9], a6, b2, iuu, pt;\n"
+      "@e tcgen05.mma.cta_group::1.kind::i8 [%9], a7, b1, ius, pt;\n"
+      "}\n" ::"r"(d[0]),
+      "l"(a0), "l"(b0), "r"(first), "r"(d[1]), "r"(d[2]), "r"(d[3]), "r"(d[4]), "r"(d[5]),
+      "r"(d[6])
       : "memory");
 }
 
