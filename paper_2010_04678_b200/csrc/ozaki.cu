@@ -94,7 +94,9 @@ __global__ void oz_slice_rows_kernel(const double* __restrict__ x, long long sm,
 }
 
 // Lo slices: ls[7][cap_pad][Kp] (column c of lo as a p-contiguous row),
-// cex[c] = scale exponent el of column c.  Block = 256 threads for columns c0..c0+31.
+// cex[c] = scale exponent el of column c.  Block (x, y) = 256 threads for
+// columns 32x..32x+31 and p-chunk y (32 values); the column max is taken
+// over all p by every chunk's block (L2-resident, 8 loads per thread).
 __global__ void oz_slice_cols_kernel(const double* __restrict__ lo, long long ld, int Dp, int Kp,
                                      const int* width_ptr, int width, long long cap_pad,
                                      uint8_t* __restrict__ ls, int* __restrict__ cex) {
@@ -102,15 +104,19 @@ __global__ void oz_slice_cols_kernel(const double* __restrict__ lo, long long ld
   __shared__ double red[8][33];
   __shared__ int ex[32];
   const int W = width_ptr ? *width_ptr : width;
-  const int c0 = blockIdx.x * 32;
+  const int c0 = blockIdx.x * 32, p0 = blockIdx.y * 32;
   if (c0 >= W) return;
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int c = c0 + lane;
   {
-    const int c = c0 + lane;
     double mx = 0.0;
     if (c < W)
       for (int p = w; p < Dp; p += 8) mx = fmax(mx, fabs(lo[(long long)p * ld + c]));
     red[w][lane] = mx;
+  }
+  for (int pp = w; pp < 32; pp += 8) {
+    const int p = p0 + pp;
+    tile[pp][lane] = (c < W && p < Dp) ? lo[(long long)p * ld + c] : 0.0;
   }
   __syncthreads();
   if (w == 0) {
@@ -119,27 +125,16 @@ __global__ void oz_slice_cols_kernel(const double* __restrict__ lo, long long ld
     for (int k = 1; k < 8; ++k) v = fmax(v, red[k][lane]);
     const int e = scale_exp(v);
     ex[lane] = e;
-    if (c0 + lane < W) cex[c0 + lane] = e;
+    if (blockIdx.y == 0 && c < W) cex[c] = e;
   }
   __syncthreads();
   const size_t slice_stride = size_t(cap_pad) * size_t(Kp);
-  for (int p0 = 0; p0 < Kp; p0 += 32) {
-    {
-      const int c = c0 + lane;
-      for (int pp = w; pp < 32; pp += 8) {
-        const int p = p0 + pp;
-        tile[pp][lane] = (c < W && p < Dp) ? lo[(long long)p * ld + c] : 0.0;
-      }
-    }
-    __syncthreads();
-    for (int cc = w; cc < 32; cc += 8) {
-      uint8_t s[kSlices];
-      slice7(tile[lane][cc], ex[cc], s);
-      uint8_t* dst = ls + size_t(c0 + cc) * size_t(Kp) + p0 + lane;
+  for (int cc = w; cc < 32; cc += 8) {
+    uint8_t sl[kSlices];
+    slice7(tile[lane][cc], ex[cc], sl);
+    uint8_t* dst = ls + size_t(c0 + cc) * size_t(Kp) + p0 + lane;
 #pragma unroll
-      for (int k = 0; k < kSlices; ++k) dst[k * slice_stride] = s[k];
-    }
-    __syncthreads();
+    for (int k = 0; k < kSlices; ++k) dst[k * slice_stride] = sl[k];
   }
 }
 
@@ -290,7 +285,8 @@ int launch_contraction_ozaki(Tensor& t, const ModePlan& p, int key, const double
       (reinterpret_cast<uintptr_t>(ls + size_t(kSlices) * cap_pad * o.Kp) + 255) & ~uintptr_t(255));
   const int sms = sm_count(t.device);
 
-  oz_slice_cols_kernel<<<(unsigned)((cap + 31) / 32), 256, 0, stream>>>(
+  oz_slice_cols_kernel<<<dim3((unsigned)((cap + 31) / 32), (unsigned)(o.Kp / 32)), 256, 0,
+                         stream>>>(
       lo, lo_ld, (int)std::min<long long>(lrows, p.Dp), (int)o.Kp, width_ptr, width, cap_pad, ls,
       cex);
   CALS_CUDA_TRY(cudaGetLastError());

@@ -97,32 +97,19 @@ __host__ __device__ constexpr uint32_t idesc_i8(int a_signed, int b_signed) {
          ((uint32_t)(BNM >> 3) << 17) | ((uint32_t)(BMC >> 4) << 24);
 }
 // ------------------------------------------------------------------ slicing --
-// v in (-2^e, 2^e): 7 slices, s1 signed, s2..s7 unsigned (see header).
-// |v| < 2^(e-55) is below the last slice and becomes 0: for a tiny negative
-// v, floor would give s1 = -1 and r = 1 + t, which rounds to exactly 1.0
-// when |t| < 2^-53 (the one inexact step of the split) and would turn into
-// a -2^(e-7) error.  Above the flush threshold r < 1 - 2^-48 and every
-// slice stays in range; the clamp is a second guard.
+// v in (-2^e, 2^e): 7 slices, s1 signed, s2..s7 unsigned (see header).  The
+// slices are the base-256 digits of Y = floor(v 2^(55-e)) (|Y| < 2^55): the
+// scaling is by a power of two and floor is exact, so one multiply and one
+// conversion give all seven exactly (the top digit as a signed byte).
 __device__ __forceinline__ void slice7(double v, int e, uint8_t (&s)[kSlices]) {
-  double t = ldexp(v, 7 - e);
-  if (fabs(t) < 0x1p-48) t = 0.0;
-  double f = floor(t);
-  s[0] = (uint8_t)(int8_t)(int)f;
-  double r = t - f;
+  const int k = 55 - e;
+  const double t = (k >= -1022 && k <= 1023) ? v * __hiloint2double((k + 1023) << 20, 0)
+                                             : ldexp(v, k);
+  const long long y = __double2ll_rd(t);
+  s[0] = (uint8_t)(y >> 48);
 #pragma unroll
-  for (int k = 1; k < kSlices; ++k) {
-    t = r * 256.0;
-    f = fmin(floor(t), 255.0);
-    s[k] = (uint8_t)(int)f;
-    r = t - f;
-  }
+  for (int i = 1; i < kSlices; ++i) s[i] = (uint8_t)(y >> (48 - 8 * i));
 }
-// (double)(int32)v exactly, on the FP64 pipe instead of the (quarter-rate)
-// conversion unit: the double 2^52 + 2^31 + v minus 2^52 + 2^31
-__device__ __forceinline__ double i2d_exact(uint32_t v) {
-  return __hiloint2double(0x43300000, (int)(v ^ 0x80000000u)) - 4503601774854144.0;
-}
-
 // smallest e with max|v| < 2^e (0 for an all-zero vector)
 __device__ __forceinline__ int scale_exp(double amax) { return amax > 0.0 ? ilogb(amax) + 1 : 0; }
 
