@@ -708,6 +708,7 @@ static void rate(int sms) {
 int main() {
   int sms; cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
   bool ok = true;
+  printf("== descriptor / layout checks vs CPU integer GEMM\n");
   ok &= check<32>(1, 6, 1);
   ok &= check<32>(1, 0, 1);
   ok &= check<32>(4, 6, 0);
@@ -715,52 +716,26 @@ int main() {
   ok &= check<128>(2, 6, 0);
   ok &= check<16>(2, 6, 1);
   if (!ok) printf("DESCRIPTOR CHECK FAILED\n");
+  printf("== MMA instruction rate (M=128, K=32, G accumulators, all SMs)\n");
+  rate<16, 7, false>(sms);
+  rate<32, 7, false>(sms);
+  rate<48, 7, false>(sms);
+  rate<64, 7, false>(sms);
+  rate<128, 3, false>(sms);
+  rate<256, 1, false>(sms);
+  rate<16, 7, true>(sms);
+  rate<32, 7, true>(sms);
+  rate<64, 4, true>(sms);
+  printf("== Ozaki pattern (28 products, 7 accumulators), issue warps, pipeline ping-pong\n");
+  pattern_rate<64, false>(sms);
+  multi_rate<64, 1>(sms);
+  multi_rate<64, 2>(sms);
+  pipe_rate<64, 2>(sms);
+  pipe_rate<64, 3>(sms);
+  printf("== other pipes concurrent with the INT8 MMA stream (time alone / MMA alone / both)\n");
   dfma_mma_test<0>(sms);
   dfma_mma_test<1>(sms);
   dfma_mma_test<2>(sms);
   dfma_mma_test<3>(sms);
-  return 0;
-  pipe_rate<64, 1>(sms);
-  pipe_rate<64, 2>(sms);
-  pipe_rate<64, 3>(sms);
-  pipe_rate<64, 4>(sms);
-  multi_rate<64, 1>(sms);
-  multi_rate<64, 2>(sms);
-  multi_rate<64, 4>(sms);
-  multi_rate<32, 1>(sms);
-  multi_rate<32, 2>(sms);
-  multi_rate<32, 4>(sms);
-  multi_rate<16, 4>(sms);
-  return 0;
-  pattern_rate<64, false>(sms);
-  pattern_rate<64, true>(sms);
-  pattern_rate<48, true>(sms);
-  pattern_rate<32, true>(sms);
-  rate<16, 7, false>(sms);
-  rate<32, 7, false>(sms);
-  rate<64, 7, false>(sms);
-  rate<128, 3, false>(sms);
-  rate<256, 1, false>(sms);
-
-  rate<48, 7, false>(sms);
-
-  rate<16, 7, true>(sms);
-  rate<32, 7, true>(sms);
-  rate<64, 4, true>(sms);
-  {
-    int* sink; CK(cudaMalloc(&sink, 4));
-    cudaEvent_t e0, e1; cudaEventCreate(&e0); cudaEventCreate(&e1);
-    tmem_rate<<<sms, 128>>>(10, sink);
-    CK(cudaDeviceSynchronize());
-    const int iters = 2000;
-    cudaEventRecord(e0);
-    tmem_rate<<<sms, 128>>>(iters, sink);
-    cudaEventRecord(e1);
-    CK(cudaDeviceSynchronize());
-    float ms; cudaEventElapsedTime(&ms, e0, e1);
-    int clk; cudaDeviceGetAttribute(&clk, cudaDevAttrClockRate, 0);
-    double bytes = (double)sms * iters * 512 * 128 * 4;
-    printf("tmem_ld: %.3f ms  %.0f B/clk/SM\n", ms, bytes / sms / (ms * 1e-3 * clk * 1e3));
-  }
   return 0;
 }
