@@ -645,6 +645,7 @@ struct Engine {
   int move_grid = 0;
   cudaGraph_t graph = nullptr;
   cudaGraphExec_t exec = nullptr;
+  bool graph_stale = false;  // tensor re-bound since the capture
   cudaStream_t cap_stream = nullptr;
   int trace_cap = 0;
   int last_iterations = 0;
@@ -1105,7 +1106,7 @@ static int engine_set_line_search(Engine* e, int enabled, double alpha) {
 }
 
 static int engine_capture(Engine* e, cudaStream_t stream) {
-  if (e->exec) return kOk;
+  if (e->exec && !e->graph_stale) return kOk;
   // capture on a private stream (the caller's stream may be the legacy default stream)
   cudaStream_t cs;
   CALS_CUDA_TRY(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
@@ -1119,8 +1120,24 @@ static int engine_capture(Engine* e, cudaStream_t stream) {
     return rc;
   }
   CALS_CUDA_TRY(ce);
+  if (e->exec) {
+    // stale graph (new tensor): update the instantiated graph in place
+    cudaGraphExecUpdateResultInfo info;
+    if (cudaGraphExecUpdate(e->exec, g, &info) == cudaSuccess) {
+      if (e->graph) cudaGraphDestroy(e->graph);
+      e->graph = g;
+      e->graph_stale = false;
+      return kOk;
+    }
+    (void)cudaGetLastError();
+    cudaGraphExecDestroy(e->exec);
+    e->exec = nullptr;
+    if (e->graph) cudaGraphDestroy(e->graph);
+    e->graph = nullptr;
+  }
   e->graph = g;
   CALS_CUDA_TRY(cudaGraphInstantiate(&e->exec, g, 0));
+  e->graph_stale = false;
   (void)stream;
   return kOk;
 }
@@ -1408,11 +1425,10 @@ int cals_engine_set_tensor(cals_engine* e, cals_tensor* t) {
   if (t->t->uid != g->tensor_uid) {
     g->t = t->t;
     g->tensor_uid = t->t->uid;
-    // the captured graph embeds the old tensor's TMA descriptors
-    if (g->exec) cudaGraphExecDestroy(g->exec);
-    if (g->graph) cudaGraphDestroy(g->graph);
-    g->exec = nullptr;
-    g->graph = nullptr;
+    // the captured graph embeds the old tensor's TMA descriptors (and Ozaki
+    // slices): re-captured at the next run and swapped into the executable
+    // graph by cudaGraphExecUpdate (same topology, new kernel parameters)
+    g->graph_stale = true;
   }
   return kOk;
 }
