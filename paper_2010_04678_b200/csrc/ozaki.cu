@@ -31,7 +31,7 @@ __global__ void oz_slice_rows_kernel(const double* __restrict__ x, long long sm,
     const int m = m0 + lane;
     double mx = 0.0;
     if (m < M)
-      for (int p = w; p < Dp; p += 8) mx = fmax(mx, fabs(xq[m + (long long)p * sp]));
+      for (int p = w; p < Dp; p += 8) mx = fmax(mx, abs_or_inf(xq[m + (long long)p * sp]));
     red[w][lane] = mx;
     __syncthreads();
     if (w == 0) {
@@ -45,7 +45,8 @@ __global__ void oz_slice_rows_kernel(const double* __restrict__ x, long long sm,
       const int m = m0 + r;
       double v = 0.0;
       if (m < M)
-        for (int p = lane; p < Dp; p += 32) v = fmax(v, fabs(xq[(long long)m * sm + (long long)p * sp]));
+        for (int p = lane; p < Dp; p += 32)
+          v = fmax(v, abs_or_inf(xq[(long long)m * sm + (long long)p * sp]));
 #pragma unroll
       for (int o = 16; o; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
       if (lane == 0) red[0][r] = v;
@@ -53,13 +54,14 @@ __global__ void oz_slice_rows_kernel(const double* __restrict__ x, long long sm,
   }
   __syncthreads();
   if (w == 0) {
-    const int e = scale_exp(red[0][lane]);
+    const int e = scale_exp_checked(red[0][lane]);
     ex[lane] = e;
     const int m = m0 + lane;
     if (m < M) {
       rex[(long long)q * M + m] = e;
-      // the epilogue scales by exponent-field adds: keep |ex| <= 900
-      if (e < -900 || e > 900) atomicOr(out_of_range, 1);
+      // the epilogue scales by exponent-field adds: keep |ex| <= 900; a
+      // non-finite tensor entry sends the whole view to the DMMA kernel
+      if (e == kNonFinite || e < -900 || e > 900) atomicOr(out_of_range, 1);
     }
   }
   __syncthreads();
@@ -111,7 +113,7 @@ __global__ void oz_slice_cols_kernel(const double* __restrict__ lo, long long ld
   {
     double mx = 0.0;
     if (c < W)
-      for (int p = w; p < Dp; p += 8) mx = fmax(mx, fabs(lo[(long long)p * ld + c]));
+      for (int p = w; p < Dp; p += 8) mx = fmax(mx, abs_or_inf(lo[(long long)p * ld + c]));
     red[w][lane] = mx;
   }
   for (int pp = w; pp < 32; pp += 8) {
@@ -123,7 +125,7 @@ __global__ void oz_slice_cols_kernel(const double* __restrict__ lo, long long ld
     double v = red[0][lane];
 #pragma unroll
     for (int k = 1; k < 8; ++k) v = fmax(v, red[k][lane]);
-    const int e = scale_exp(v);
+    const int e = scale_exp_checked(v);
     ex[lane] = e;
     if (blockIdx.y == 0 && c < W) cex[c] = e;
   }
@@ -226,7 +228,8 @@ int ozaki_prepare(Tensor& t, const ModePlan& p, int key, cudaStream_t stream) {
   oz_slice_rows_kernel<<<grid, 256, 0, stream>>>(t.data, sm, sp, sq, (int)p.M, (int)p.Dp,
                                                  (int)o.Kp, (int)p.Dq, o.xs, o.rex, flag);
   CALS_CUDA_TRY(cudaGetLastError());
-  // once per tensor and view: a tensor with rows beyond 2^+-900 stays on DMMA
+  // once per tensor and view: a tensor with rows beyond 2^+-900 or with a
+  // non-finite entry stays on DMMA
   int h_flag = 0;
   CALS_CUDA_TRY(cudaMemcpyAsync(&h_flag, flag, sizeof(int), cudaMemcpyDeviceToHost, stream));
   CALS_CUDA_TRY(cudaStreamSynchronize(stream));

@@ -110,8 +110,21 @@ __device__ __forceinline__ void slice7(double v, int e, uint8_t (&s)[kSlices]) {
 #pragma unroll
   for (int i = 1; i < kSlices; ++i) s[i] = (uint8_t)(y >> (48 - 8 * i));
 }
+// Lo columns holding a NaN or Inf get this scale exponent: their slices are
+// zero and the epilogue emits NaN for them (as the FP64 contraction would).
+// A tensor with a non-finite entry is left to the DMMA kernel.
+constexpr int kNonFinite = 1 << 20;
+__device__ __forceinline__ double abs_or_inf(double v) {
+  const double a = fabs(v);
+  return a <= 1.7976931348623157e308 ? a : __longlong_as_double(0x7ff0000000000000LL);
+}
+__device__ __forceinline__ int scale_exp_checked(double amax);
+
 // smallest e with max|v| < 2^e (0 for an all-zero vector)
 __device__ __forceinline__ int scale_exp(double amax) { return amax > 0.0 ? ilogb(amax) + 1 : 0; }
+__device__ __forceinline__ int scale_exp_checked(double amax) {
+  return amax <= 1.7976931348623157e308 ? scale_exp(amax) : kNonFinite;
+}
 
 __device__ __forceinline__ void unit_decode(int u, int tn, int tm, int& tile_c, int& tile_m,
                                             int& s) {
@@ -304,8 +317,10 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int c = tc * BMC + quad * 32 + lane;
       const bool cval = c < W;
       const int mb = tmi * BNM + half * 32;
-      const int kside = cval ? args.cex[c] - 50 : 0;
-      const double cscale = cval ? pow2(kside) : 0.0;
+      const int el = cval ? args.cex[c] : 0;
+      const int kside = el - 50;
+      const double kNaN = __longlong_as_double(0x7ff8000000000000LL);
+      const double cscale = !cval ? 0.0 : (el == kNonFinite ? kNaN : pow2(kside));
       // exponent-add fast path for the side output: |ex| <= 900 and the
       // result exponent field e_P + ex + kside (e_P in [1023, 1085]) in range
       const bool side_fast = __all_sync(0xffffffffu, kside >= -122 && kside <= 61);
@@ -372,7 +387,8 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
           for (int j = 0; j < 32; ++j) {
             const int m = mb + j;
-            const double y = exp_add(P[j], __shfl_sync(0xffffffffu, rex_lane, j));
+            const int ex = __shfl_sync(0xffffffffu, rex_lane, j);
+            const double y = exp_add(P[j], ex);
             if (args.side && cval && m < args.M)
               __stcg(args.side + ((long long)m + args.side_qstride * q) * args.ld_side + c,
                      y * cscale);

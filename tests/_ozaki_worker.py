@@ -32,7 +32,8 @@ def main():
     out = {"cases": []}
     cases = [((200, 200, 200), 300, "normal"), ((160, 130, 150), 129, "uniform"),
              ((256, 144, 96), 64, "range"), ((150, 140, 20), 1, "normal"),
-             ((130, 200, 70), 257, "zeros")]
+             ((130, 200, 70), 257, "zeros"), ((140, 136, 132), 40, "nonfinite"),
+             ((150, 140, 130), 33, "nonfinite_tensor")]
     for dims, width, kind in cases:
         if kind == "uniform":
             arr = rng.random(dims)
@@ -48,13 +49,26 @@ def main():
             for f in fac:
                 f[:, ::5] = 0.0
             arr[:, 3, :] = 0.0
+        if kind == "nonfinite":  # NaN / Inf in factor columns (non-finite tensors: DMMA path)
+            fac[0][5, 3] = np.nan
+            fac[2][7, 11] = np.nan
+            fac[1][9, 30] = np.inf
+        if kind == "nonfinite_tensor":  # an Inf tensor entry: the view falls back to DMMA
+            arr[17, 4, 9] = np.inf
         fac = [np.asfortranarray(f) for f in fac]
         t = cals.DenseTensor.from_array(arr)
         ws = cals.MttkrpWorkspace(dims, width)
         errs = []
         for n in range(len(dims)):
             got = np.array(cals.mttkrp(t, fac, n, ws=ws))
-            errs.append(rel(got, ref_mttkrp(arr, fac, n)))
+            want = ref_mttkrp(arr, fac, n)
+            if kind.startswith("nonfinite"):
+                # same non-finite pattern, finite entries within tolerance
+                same = bool(np.array_equal(np.isfinite(got), np.isfinite(want)))
+                ok = np.isfinite(want)
+                errs.append(rel(got[ok], want[ok]) if same else 1.0)
+            else:
+                errs.append(rel(got, want))
         out["cases"].append({"dims": dims, "width": width, "kind": kind, "rel": errs})
 
     # bitwise: duplicated columns, and a block of columns at two offsets
