@@ -402,7 +402,13 @@ def main_gpu(args) -> None:
            "models_this_gpu": n_models, "r_star": r_star,
            "parallelism": f"model-batch x{world}, tensor replicated, no collective",
            "l2": "flushed between steps (256 MiB write)",
-           "driver_iterations_per_step": it_mean}
+           "driver_iterations_per_step": it_mean,
+           "mttkrp_kernels": {f"mode{n}": ("int8-ozaki" if k == 1 else "fp64-dmma")
+                              for n, k in enumerate(kinds)},
+           "tensor_slices": "the INT8 path's tensor slices (a derived format of the immutable "
+                            "tensor) are built once per tensor: outside the timed steps of "
+                            "`value` (tensor resident), inside every step of `e2e` (fresh "
+                            "tensor per run)"}
     if wl["tol"] <= 0:  # reference flop model (driver.py:124-125) over the sweep
         cfg["sweep_mttkrp_tflops_reference_model"] = 3 * wl["iters"] * 2 * sum(
             m.rank for m in models) * float(np.prod(dims)) / (ms_max * 1e-3) / 1e12
