@@ -38,7 +38,8 @@ struct OzSlices {
   uint8_t* xs = nullptr;
   int* rex = nullptr;
   long long Kp = 0, M = 0, Dq = 0, Dp = 0;
-  CUtensorMap map;
+  CUtensorMap map;   // full 64-row tiles
+  CUtensorMap rmap;  // packed remainder tiles (== map when unused)
 };
 
 // Device-resident dense tensor, mode-0 fastest, I0 padded to even so every

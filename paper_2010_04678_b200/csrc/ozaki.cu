@@ -185,11 +185,23 @@ bool ozaki_eligible(const ModePlan& p) {
   return p.Dp >= 128 && m_fill * k_fill >= 0.6 && p.Dq >= 3LL * p.S;
 }
 
+// m tiling (see Args): full 64-row tiles plus, when the M % 64 leftover rows
+// of a q-split's slabs fit one tile, a packed remainder tile per split
+struct MTiling {
+  int tm_full, rem_rows, rem_slabs;
+};
+static MTiling m_tiling(const ModePlan& p) {
+  const long long r = p.M % BNM, nslab = (p.Dq + p.S - 1) / p.S;
+  if (r > 0 && r * nslab <= BNM) return {int(p.M / BNM), int(r), int(nslab)};
+  return {int((p.M + BNM - 1) / BNM), 0, 0};
+}
+
 // 28 slice products x 2 ops per MAC over the padded tiles the kernel runs
 double ozaki_tensor_ops(const ModePlan& p, long long width) {
-  const double mp = double((p.M + BNM - 1) / BNM * BNM);
+  const MTiling mt = m_tiling(p);
   const double wp = double((width + BMC - 1) / BMC * BMC);
-  return 2.0 * 28.0 * mp * wp * double(kp_of(p.Dp)) * double(p.Dq);
+  const double tile_passes = double(mt.tm_full) * double(p.Dq) + (mt.rem_rows ? double(p.S) : 0.0);
+  return 2.0 * 28.0 * double(BNM) * tile_passes * wp * double(kp_of(p.Dp));
 }
 
 size_t ozaki_ws_bytes(const ModePlan& p, long long cap) {
@@ -246,6 +258,14 @@ int ozaki_prepare(Tensor& t, const ModePlan& p, int key, cudaStream_t stream) {
     const uint32_t box[4] = {KSTEP, BNM, 1, kSlices};
     int rc = encode_map_u8(&o.map, o.xs, 4, dims, strides, box);
     if (rc) return rc;
+    const MTiling mt = m_tiling(p);
+    if (mt.rem_rows) {  // packed remainder tiles: rows M-r.., rem_slabs slabs, one slice
+      const uint32_t rbox[4] = {KSTEP, (uint32_t)mt.rem_rows, (uint32_t)mt.rem_slabs, 1};
+      rc = encode_map_u8(&o.rmap, o.xs, 4, dims, strides, rbox);
+      if (rc) return rc;
+    } else {
+      o.rmap = o.map;
+    }
   }
   std::lock_guard<std::mutex> lk(t.mu);
   if (t.oz.count(key)) {  // another thread raced us: keep theirs
@@ -319,6 +339,10 @@ int launch_contraction_ozaki(Tensor& t, const ModePlan& p, int key, const double
   a.side = side;
   a.ld_side = side_ld;
   a.side_qstride = side_qstride;
+  const MTiling mt = m_tiling(p);
+  a.tm_full = mt.tm_full;
+  a.rem_rows = mt.rem_rows;
+  a.rem_slabs = mt.rem_slabs;
   static const int dbg = getenv("CALS_OZ_DBG") ? atoi(getenv("CALS_OZ_DBG")) : 0;
   a.dbg = dbg;
   static unsigned long long* prof = nullptr;
@@ -351,9 +375,10 @@ int launch_contraction_ozaki(Tensor& t, const ModePlan& p, int key, const double
                                     (int)kSmemBytes);
   });
   CALS_CUDA_TRY(attr_err);
-  const long long units = ((cap + BMC - 1) / BMC) * ((p.M + BNM - 1) / BNM) * p.S;
+  const long long units =
+      ((cap + BMC - 1) / BMC) * (mt.tm_full + (mt.rem_rows ? 1 : 0)) * (long long)p.S;
   dim3 grid((unsigned)std::max<long long>(1, std::min<long long>(units, sms)));
-  mttkrp_ozaki_kernel<<<grid, kThreads, kSmemBytes, stream>>>(o.map, mapL, a);
+  mttkrp_ozaki_kernel<<<grid, kThreads, kSmemBytes, stream>>>(o.map, mapL, o.rmap, a);
   CALS_CUDA_TRY(cudaGetLastError());
   if (p.S > 1) {
     const long long pairs = p.M * ((cap + 1) / 2);

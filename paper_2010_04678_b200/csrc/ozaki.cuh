@@ -86,6 +86,13 @@ struct Args {
   double* side;      // optional per-slab products side[(m + side_qstride q) * ld_side + c]
   long long ld_side;
   long long side_qstride;
+  // m tiling: tm_full tiles of 64 rows; if rem_rows > 0 the last M % 64 rows
+  // of every slab of a q-split are packed into ONE extra 64-row tile
+  // (rem_rows x rem_slabs rows, slab-major), so a 200-row mode costs 3 + 1/6
+  // instead of 4 tile passes per slab.
+  int tm_full;
+  int rem_rows;
+  int rem_slabs;
   int dbg;           // timing experiments only: 1 = no TMA, 2 = no epilogue math
   unsigned long long* prof;  // dbg & 8: per-CTA {total, wait_full, wait_tempty} cycles
 };
@@ -126,12 +133,23 @@ __device__ __forceinline__ int scale_exp_checked(double amax) {
   return amax <= 1.7976931348623157e308 ? scale_exp(amax) : kNonFinite;
 }
 
-__device__ __forceinline__ void unit_decode(int u, int tn, int tm, int& tile_c, int& tile_m,
-                                            int& s) {
-  tile_c = u % tn;
+// Work unit u (c fastest): a full 64-row m-tile over the slabs of one q-split,
+// or the split's packed remainder tile (one pass, rem_rows x slabs rows).
+struct Unit {
+  int tc, s, qb, qe, m0;
+  bool rem;
+};
+__device__ __forceinline__ Unit unit_decode(int u, int tn, const Args& a) {
+  Unit U;
+  U.tc = u % tn;
   const int t = u / tn;
-  tile_m = t % tm;
-  s = t / tm;
+  const int full = a.tm_full * a.S;
+  U.rem = t >= full;
+  U.s = U.rem ? t - full : t / a.tm_full;
+  U.m0 = U.rem ? a.M - a.rem_rows : (t % a.tm_full) * BNM;
+  U.qb = int((long long)U.s * a.Dq / a.S);
+  U.qe = int((long long)(U.s + 1) * a.Dq / a.S);
+  return U;
 }
 
 // v * 2^k for v = (double) of an integer (0 or |v| in [1, 2^62)) and an
@@ -148,10 +166,48 @@ __device__ __forceinline__ double pow2(int e) {
   return __hiloint2double((e + 1023) << 20, 0);
 }
 
+// Epilogue: drain one pass's 7 group accumulators (each TMEM buffer released
+// to the MMA warp as soon as it is in registers) and recombine them in 64-bit
+// integers into P (the double of Q ~ P' / 2^12, see the kernel comment).
+__device__ __forceinline__ void drain_pass(uint64_t* tfull, uint64_t* tempty, uint32_t slab,
+                                           uint32_t trow, int lane, double (&P)[32],
+                                           long long& ew_wait, long long& ew_load) {
+  uint32_t v[32];
+  long long Qv[32];
+#pragma unroll
+  for (int g = 0; g < kGroups; ++g) {
+    const long long e0 = clock64();
+    const uint32_t L = 7u * slab + g, buf = L & 7u;
+    mbar_wait(&tfull[buf], (L >> 3) & 1u);
+    tc_fence_after();
+    const long long e1 = clock64();
+    ew_wait += e1 - e0;
+    tmem_ld32(trow + buf * BNM, v);
+    tc_fence_before();
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&tempty[buf]);  // TMEM buffer free for its next use
+    ew_load += clock64() - e1;
+    if (g == 0) {
+#pragma unroll
+      for (int j = 0; j < 32; ++j) Qv[j] = (long long)(int)v[j];
+    } else if (g <= 4) {
+#pragma unroll
+      for (int j = 0; j < 32; ++j) Qv[j] = Qv[j] * 256 + (long long)(int)v[j];
+    } else if (g == 5) {
+#pragma unroll
+      for (int j = 0; j < 32; ++j) Qv[j] = Qv[j] * 16 + (long long)((int)v[j] >> 4);
+    } else {
+#pragma unroll
+      for (int j = 0; j < 32; ++j) P[j] = (double)(Qv[j] + (long long)((int)v[j] >> 12));
+    }
+  }
+}
+
 // ------------------------------------------------------------- main kernel --
 __global__ void __launch_bounds__(kThreads, 1)
     mttkrp_ozaki_kernel(const __grid_constant__ CUtensorMap tmX,
-                        const __grid_constant__ CUtensorMap tmL, const Args args) {
+                        const __grid_constant__ CUtensorMap tmL,
+                        const __grid_constant__ CUtensorMap tmR, const Args args) {
   // dynamic shared memory starts at the CTA window base (no static smem in
   // this kernel): 1024-byte aligned, as the 32-byte swizzle atoms need.  No
   // pointer arithmetic through integers, so accesses stay LDS/STS.
@@ -167,8 +223,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int W = args.width_ptr ? *args.width_ptr : args.width;
   if (W <= 0) return;
   const int tn = (W + BMC - 1) / BMC;
-  const int tm = (args.M + BNM - 1) / BNM;
-  const int units = tn * tm * args.S;
+  const int units = tn * (args.tm_full + (args.rem_rows ? 1 : 0)) * args.S;
   if ((int)blockIdx.x >= units) return;
   const int KS = args.KS;
 
@@ -202,23 +257,35 @@ __global__ void __launch_bounds__(kThreads, 1)
       tma_prefetch_desc(&tmL);
       int stage = 0;
       uint32_t phase = 0;
+      tma_prefetch_desc(&tmR);
+      const uint32_t rem_tx =
+          uint32_t(kLoStageBytes + kSlices * KSTEP * args.rem_rows * args.rem_slabs);
       for (int u = blockIdx.x; u < units; u += gridDim.x) {
-        int tc, tmi, s;
-        unit_decode(u, tn, tm, tc, tmi, s);
-        const int qb = int((long long)s * args.Dq / args.S);
-        const int qe = int((long long)(s + 1) * args.Dq / args.S);
-        for (int q = qb; q < qe; ++q) {
+        const Unit U = unit_decode(u, tn, args);
+        const int passes = U.rem ? 1 : U.qe - U.qb;
+        for (int i = 0; i < passes; ++i) {
+          const int q = U.qb + i;
           for (int ks = 0; ks < KS; ++ks) {
             mbar_wait(&empty[stage], phase ^ 1u);
             unsigned char* st = smem + size_t(stage) * kStageBytes;
-            if ((args.dbg & 1) && (q > qb + 1)) {
+            if ((args.dbg & 1) && (i > 1)) {
               mbar_arrive(&full[stage]);
               if (++stage == STAGES) { stage = 0; phase ^= 1u; }
               continue;
             }
-            mbar_arrive_expect_tx(&full[stage], kStageBytes);
-            tma_load_3d(st, &tmL, &full[stage], ks * KSTEP, tc * BMC, 0);
-            tma_load_4d(st + kLoStageBytes, &tmX, &full[stage], ks * KSTEP, tmi * BNM, q, 0);
+            if (U.rem) {
+              // rows M-r..M-1 of slabs qb.. (rem_slabs of them), one box per
+              // slice at the slice's 2048-byte B-tile offset
+              mbar_arrive_expect_tx(&full[stage], rem_tx);
+              tma_load_3d(st, &tmL, &full[stage], ks * KSTEP, U.tc * BMC, 0);
+              for (int j = 0; j < kSlices; ++j)
+                tma_load_4d(st + kLoStageBytes + j * kXTileBytes, &tmR, &full[stage], ks * KSTEP,
+                            U.m0, U.qb, j);
+            } else {
+              mbar_arrive_expect_tx(&full[stage], kStageBytes);
+              tma_load_3d(st, &tmL, &full[stage], ks * KSTEP, U.tc * BMC, 0);
+              tma_load_4d(st + kLoStageBytes, &tmX, &full[stage], ks * KSTEP, U.m0, q, 0);
+            }
             if (++stage == STAGES) { stage = 0; phase ^= 1u; }
           }
         }
@@ -237,11 +304,9 @@ __global__ void __launch_bounds__(kThreads, 1)
     long long w_full = 0, w_tempty = 0;
     const long long t_start = clock64();
     for (int u = blockIdx.x; u < units; u += gridDim.x) {
-      int tc, tmi, s;
-      unit_decode(u, tn, tm, tc, tmi, s);
-      const int qb = int((long long)s * args.Dq / args.S);
-      const int qe = int((long long)(s + 1) * args.Dq / args.S);
-      for (int q = qb; q < qe; ++q, ++slab) {
+      const Unit U = unit_decode(u, tn, args);
+      const int passes = U.rem ? 1 : U.qe - U.qb;
+      for (int i = 0; i < passes; ++i, ++slab) {
         for (int ks = 0; ks < KS; ++ks) {
           long long t0 = clock64();
           mbar_wait(&full[stage], phase);
@@ -310,13 +375,10 @@ __global__ void __launch_bounds__(kThreads, 1)
     long long ew_wait = 0, ew_load = 0, ew_final = 0;
     const long long e_start = clock64();
     for (int u = blockIdx.x; u < units; u += gridDim.x) {
-      int tc, tmi, s;
-      unit_decode(u, tn, tm, tc, tmi, s);
-      const int qb = int((long long)s * args.Dq / args.S);
-      const int qe = int((long long)(s + 1) * args.Dq / args.S);
-      const int c = tc * BMC + quad * 32 + lane;
+      const Unit U = unit_decode(u, tn, args);
+      const int c = U.tc * BMC + quad * 32 + lane;
       const bool cval = c < W;
-      const int mb = tmi * BNM + half * 32;
+      const int mb = U.m0 + half * 32;
       const int el = cval ? args.cex[c] : 0;
       const int kside = el - 50;
       const double kNaN = __longlong_as_double(0x7ff8000000000000LL);
@@ -327,83 +389,93 @@ __global__ void __launch_bounds__(kThreads, 1)
       // this thread's accumulator column in shared memory (touched once per
       // slab; keeps the registers for the TMEM values)
       double* acc = acc_s + (threadIdx.x - 64);
+      // Drain this pass's 7 group accumulators (each released to the MMA warp
+      // as soon as it is in registers) and recombine them into P (see above).
+      double P[32];
+      if (!U.rem) {
 #pragma unroll
-      for (int j = 0; j < 32; ++j) acc[j * 32 * kEpiWarps] = 0.0;
-      for (int q = qb; q < qe; ++q, ++slab) {
-        const double hc = cval ? __ldg(args.hi + (long long)q * args.ldh + c) * cscale : 0.0;
-        // row scales of this warp's 32 rows: one coalesced load, broadcast
-        // by shuffles (its latency hides behind the group drain)
-        const int rex_lane =
-            mb + lane < args.M ? __ldg(args.rex + (long long)q * args.M + mb + lane) : 0;
-        auto drain = [&](int g, uint32_t (&v)[32]) {
-          const long long e0 = clock64();
-          const uint32_t L = 7u * slab + g, buf = L & 7u;
-          mbar_wait(&tfull[buf], (L >> 3) & 1u);
-          tc_fence_after();
-          const long long e1 = clock64();
-          ew_wait += e1 - e0;
-          tmem_ld32(trow + buf * BNM, v);
-          tc_fence_before();
-          __syncwarp();
-          if (lane == 0) mbar_arrive(&tempty[buf]);  // TMEM buffer free for its next use
-          ew_load += clock64() - e1;
-        };
-        uint32_t v[32];
-        long long Qv[32];
-        drain(0, v);
+        for (int j = 0; j < 32; ++j) acc[j * 32 * kEpiWarps] = 0.0;
+        for (int q = U.qb; q < U.qe; ++q, ++slab) {
+          const double hc = cval ? __ldg(args.hi + (long long)q * args.ldh + c) * cscale : 0.0;
+          // row scales of this warp's 32 rows: one coalesced load, broadcast
+          // by shuffles (its latency hides behind the group drain)
+          const int rex_lane =
+              mb + lane < args.M ? __ldg(args.rex + (long long)q * args.M + mb + lane) : 0;
+          drain_pass(tfull, tempty, slab, trow, lane, P, ew_wait, ew_load);
+          const long long e2 = clock64();
+          // Scaling by 2^ex (row) and 2^(ex + el - 50) (side output) is an
+          // exponent-field add on the integer pipe: P is the double of an
+          // integer (0, or |P| in [1, 2^62)), row exponents are confined to
+          // [-900, 900] (ozaki_prepare falls back to DMMA otherwise) and the
+          // column term is checked per warp.  One DFMA per element is left.
+          if (side_fast) {
 #pragma unroll
-        for (int j = 0; j < 32; ++j) Qv[j] = (long long)(int)v[j];
+            for (int j = 0; j < 32; ++j) {
+              const int m = mb + j;
+              const int ex = __shfl_sync(0xffffffffu, rex_lane, j);
+              const double y = exp_add(P[j], ex);
+              if (args.side && cval && m < args.M)
+                __stcg(args.side + ((long long)m + args.side_qstride * q) * args.ld_side + c,
+                       exp_add(P[j], ex + kside));
+              acc[j * 32 * kEpiWarps] = fma(y, hc, acc[j * 32 * kEpiWarps]);
+            }
+          } else {
 #pragma unroll
-        for (int g = 1; g <= 4; ++g) {
-          drain(g, v);
-#pragma unroll
-          for (int j = 0; j < 32; ++j) Qv[j] = Qv[j] * 256 + (long long)(int)v[j];
+            for (int j = 0; j < 32; ++j) {
+              const int m = mb + j;
+              const double y = exp_add(P[j], __shfl_sync(0xffffffffu, rex_lane, j));
+              if (args.side && cval && m < args.M)
+                __stcg(args.side + ((long long)m + args.side_qstride * q) * args.ld_side + c,
+                       y * cscale);
+              acc[j * 32 * kEpiWarps] = fma(y, hc, acc[j * 32 * kEpiWarps]);
+            }
+          }
+          ew_final += clock64() - e2;
         }
-        drain(5, v);
-#pragma unroll
-        for (int j = 0; j < 32; ++j) Qv[j] = Qv[j] * 16 + (long long)((int)v[j] >> 4);
-        drain(6, v);
-        double P[32];
-#pragma unroll
-        for (int j = 0; j < 32; ++j) P[j] = (double)(Qv[j] + (long long)((int)v[j] >> 12));
-        const long long e2 = clock64();
-        // Scaling by 2^ex (row) and 2^(ex + el - 50) (side output) is an
-        // exponent-field add on the integer pipe: P is the double of an
-        // integer (0, or |P| in [1, 2^62)), row exponents are confined to
-        // [-900, 900] (ozaki_prepare falls back to DMMA otherwise) and the
-        // column term is checked per warp.  One DFMA per element is left.
-        if (side_fast) {
+        if (cval) {
+          double* out = args.out + (args.S > 1 ? (long long)U.s * args.part_stride : 0LL);
 #pragma unroll
           for (int j = 0; j < 32; ++j) {
             const int m = mb + j;
-            const int ex = __shfl_sync(0xffffffffu, rex_lane, j);
-            const double y = exp_add(P[j], ex);
-            if (args.side && cval && m < args.M)
-              __stcg(args.side + ((long long)m + args.side_qstride * q) * args.ld_side + c,
-                     exp_add(P[j], ex + kside));
-            acc[j * 32 * kEpiWarps] = fma(y, hc, acc[j * 32 * kEpiWarps]);
-          }
-        } else {
-#pragma unroll
-          for (int j = 0; j < 32; ++j) {
-            const int m = mb + j;
-            const int ex = __shfl_sync(0xffffffffu, rex_lane, j);
-            const double y = exp_add(P[j], ex);
-            if (args.side && cval && m < args.M)
-              __stcg(args.side + ((long long)m + args.side_qstride * q) * args.ld_side + c,
-                     y * cscale);
-            acc[j * 32 * kEpiWarps] = fma(y, hc, acc[j * 32 * kEpiWarps]);
+            if (m < args.M) out[(long long)m * args.ldo + c] = acc[j * 32 * kEpiWarps];
           }
         }
-        ew_final += clock64() - e2;
-      }
-      if (cval) {
-        double* out = args.out + (args.S > 1 ? (long long)s * args.part_stride : 0LL);
+      } else {
+        // packed remainder tile: column n = half*32 + j holds slab qb + n / r,
+        // row M - r + n % r.  Each column's Hi-weighted product is parked in
+        // shared memory, then the half-0 warp of the quadrant sums the slabs
+        // of every row in ascending order (deterministic, shape-only order).
+        drain_pass(tfull, tempty, slab, trow, lane, P, ew_wait, ew_load);
+        ++slab;
+        const int r = args.rem_rows, nq = U.qe - U.qb;
 #pragma unroll
         for (int j = 0; j < 32; ++j) {
-          const int m = mb + j;
-          if (m < args.M) out[(long long)m * args.ldo + c] = acc[j * 32 * kEpiWarps];
+          const int n = half * 32 + j, ql = n / r, m = U.m0 + n % r;
+          double t = 0.0;
+          if (ql < nq) {
+            const int q = U.qb + ql;
+            const int ex = __ldg(args.rex + (long long)q * args.M + m);
+            const double y = exp_add(P[j], ex);
+            if (args.side && cval)
+              __stcg(args.side + ((long long)m + args.side_qstride * q) * args.ld_side + c,
+                     side_fast ? exp_add(P[j], ex + kside) : y * cscale);
+            if (cval) t = y * (__ldg(args.hi + (long long)q * args.ldh + c) * cscale);
+          }
+          acc[j * 32 * kEpiWarps] = t;
         }
+        asm volatile("bar.sync %0, 64;" ::"r"(1 + quad) : "memory");
+        if (half == 0 && cval) {
+          double* out = args.out + (args.S > 1 ? (long long)U.s * args.part_stride : 0LL);
+          for (int ml = 0; ml < r; ++ml) {
+            double sum = 0.0;
+            for (int ql = 0; ql < nq; ++ql) {
+              const int n = ql * r + ml;
+              sum += n < 32 ? acc[n * 32 * kEpiWarps] : acc[(n - 32) * 32 * kEpiWarps + 128];
+            }
+            out[(long long)(U.m0 + ml) * args.ldo + c] = sum;
+          }
+        }
+        asm volatile("bar.sync %0, 64;" ::"r"(1 + quad) : "memory");
       }
     }
     if ((args.dbg & 8) && lane == 0 && (warp == 2 || warp == 5)) {
