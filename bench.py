@@ -311,7 +311,8 @@ def main_gpu(args) -> None:
     e2e_times, phases = [], []
     h2d = t.data.nbytes + pool_host.nbytes
     d2h = pool_host.nbytes + n_models * (4 * 3 + 8 * 3) + 8 * sum(m.rank for m in models)
-    for i in range(args.warmup + max(2, min(args.steps, 5))):
+    n_e2e = max(3, min(args.steps, 10))
+    for i in range(args.warmup + n_e2e):
         tt = cals.DenseTensor(dims, t.data)  # fresh tensor: upload inside the timed region
         torch.cuda.synchronize()
         tic = time.perf_counter()
@@ -330,7 +331,10 @@ def main_gpu(args) -> None:
         dist.all_reduce(te, op=dist.ReduceOp.MAX)
     e2e = {"value": total_models / float(te.item()), "unit": "models/s",
            "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
-           "phases_ms": {k: 1e3 * float(np.mean([p[k] for p in phases])) for k in phases[0]}}
+           "phases_ms": {k: 1e3 * float(np.mean([p[k] for p in phases])) for k in phases[0]},
+           "samples_ms": [round(1e3 * x, 3) for x in e2e_times],
+           "timing": "wall clock per run() call (mean over the samples), device synchronised "
+                     "before and after"}
 
     # ---- roofline of the fused MTTKRP kernel at the workload's capacity width
     peak = C.c_double()

@@ -7,7 +7,7 @@ dims = (200, 200, 200)
 t = cals.generate_synthetic(dims, 20, 0.1, seed=0)
 models = cals.build_models(dims, list(range(1, 21)), 10, seed=1)
 t.pin()
-for i in range(6):
+for i in range(int(sys.argv[1]) if len(sys.argv) > 1 else 6):
     tt = cals.DenseTensor(dims, t.data)
     torch.cuda.synchronize()
     tic = time.perf_counter()
