@@ -130,11 +130,20 @@ __device__ inline void decide_model(EngState* st, int k, double e) {
 // RB > 0: fast path (every rank <= RB, rows in registers, chunked Gram);
 // RB == 0: generic path for ranks up to 128.  Same reference semantics.
 template <int RB>
-__global__ void __launch_bounds__(kUpdThreads, 2) engine_update_kernel(EngState* st, int n,
+__global__ void __launch_bounds__(kUpdThreads, 2) engine_update_kernel(EngState* st_g, int n,
                                                                      int nthr) {
   extern __shared__ __align__(16) double dsm[];
   __shared__ int flag;
   __shared__ double red[kUpdThreads];
+  // The engine state (pointers and scalars, fixed for this launch) is read
+  // through a shared-memory copy: every st-> access in the per-model chain
+  // is then one smem load instead of a dependent global round trip.  Writes
+  // go through the copied pointers into the global arrays.
+  __shared__ __align__(16) EngState sst;
+  for (int i = threadIdx.x; i < int(sizeof(EngState) / 4); i += blockDim.x)
+    reinterpret_cast<int*>(&sst)[i] = reinterpret_cast<const int*>(st_g)[i];
+  __syncthreads();
+  EngState* const st = &sst;
   const int N = st->order;
   const int Rmax = st->max_rank;
   double* H = dsm;                // Rmax^2

@@ -293,39 +293,45 @@ struct FastPairs {
   }
 };
 
-// Upper Cholesky of H (smem, R <= 32) by warp 0, lane b owning column b;
-// row k of U is broadcast with shuffles.  U overwrites the upper triangle;
-// inv_diag[k] = 1/U[k][k].  Fails like dpotrf (pivot <= 0 or NaN).
+// Upper Cholesky of H (smem, R <= 32) by warp 0 with the matrix in
+// registers: lane b holds column b, rotated by one row per step so the
+// current pivot row is always col[0] (static register indices, compact
+// loop).  Step k: pivot from lane k, u = sqrt, inv = 1/u (uniform), row k
+// of U = H[k][b] * inv (dpotf2: DSCAL by 1/ajj), trailing update
+// H[a][b] -= U[k][a] U[k][b] with U[k][a] broadcast by shuffles.  U is
+// written back over the upper triangle; inv_diag[k] = 1/U[k][k].  Fails like
+// dpotrf (pivot <= 0 or NaN).
 __device__ inline void warp_cholesky_fast_nosync(double* __restrict__ H, int R,
                                                  double* __restrict__ inv_diag, int* flag) {
-  __shared__ double urow[32];  // row k of U, broadcast to the trailing update
-  {
-    const int lane = threadIdx.x;
-    bool ok = true;
-    for (int k = 0; k < R; ++k) {
-      const double piv = H[k * R + k];
-      if (!(piv > 0.0)) {
-        ok = false;
-        break;
-      }
-      const double u = sqrt(piv);
-      double ukb = 0.0;
-      if (lane == k) ukb = u;
-      else if (lane > k && lane < R) ukb = H[k * R + lane] / u;
-      if (lane < R) urow[lane] = ukb;
-      __syncwarp();
-      if (lane >= k && lane < R) H[k * R + lane] = ukb;
-      if (lane == k) inv_diag[k] = 1.0 / u;
-      // column `lane` of the trailing matrix: independent RMWs (no aliasing
-      // with urow), so the loads pipeline
-      if (lane > k && lane < R) {
-#pragma unroll 4
-        for (int a = k + 1; a <= lane; ++a) H[a * R + lane] = fma(-urow[a], ukb, H[a * R + lane]);
-      }
-      __syncwarp();
+  const int lane = threadIdx.x;
+  double col[32];
+#pragma unroll
+  for (int a = 0; a < 32; ++a) col[a] = (a < R && lane < R && a <= lane) ? H[a * R + lane] : 0.0;
+  bool ok = true;
+  for (int k = 0; k < R; ++k) {
+    const double piv = __shfl_sync(0xffffffffu, col[0], k);
+    if (!(piv > 0.0)) {
+      ok = false;
+      break;
     }
-    if (lane == 0) *flag = ok ? 1 : 0;
+    const double u = sqrt(piv);
+    const double inv = 1.0 / u;
+    const double ukb = lane == k ? u : (lane > k ? col[0] * inv : 0.0);
+    if (lane >= k && lane < R) H[k * R + lane] = ukb;
+    if (lane == 0) inv_diag[k] = inv;
+#pragma unroll
+    for (int a = 1; a < 32; ++a) {
+      // U[k][k + a] from lane k + a (0 past the matrix)
+      const int src = k + a;
+      const double uka = __shfl_sync(0xffffffffu, ukb, src < 32 ? src : 31);
+      if (src <= lane && src < R) col[a] = fma(-uka, ukb, col[a]);
+    }
+#pragma unroll
+    for (int a = 0; a < 31; ++a) col[a] = col[a + 1];
+    col[31] = 0.0;
   }
+  __syncwarp();
+  if (lane == 0) *flag = ok ? 1 : 0;
 }
 
 __device__ inline bool warp_cholesky_fast(double* H, int R, double* inv_diag, int* flag) {
