@@ -422,70 +422,104 @@ static UpdateKernel update_kernel_for(int max_rank, int* rb) {
 // -------------------------------------------------------------------- plan --
 // One warp: retire (registry order), compact survivors, admit FIFO with
 // head-of-line blocking (driver.py:198-208, 274-276; multimatrix.py:103-158).
-__global__ void engine_plan_kernel(EngState* st) {
+// block-wide inclusive scan of one int per thread (blockDim.x = kPlanThreads)
+constexpr int kPlanThreads = 1024;
+__device__ __forceinline__ int plan_scan(int v, int* wtot, int* total) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  int incl = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int t = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += t;
+  }
+  if (lane == 31) wtot[w] = incl;
+  __syncthreads();
+  if (w == 0) {
+    int t = wtot[lane];
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int u = __shfl_up_sync(0xffffffffu, t, o);
+      if (lane >= o) t += u;
+    }
+    wtot[lane] = t;  // inclusive over warps
+  }
+  __syncthreads();
+  const int r = incl + (w > 0 ? wtot[w - 1] : 0);
+  *total = wtot[31];
+  __syncthreads();
+  return r;
+}
+
+// Retire / compact / admit (driver.py:199-208, 274-276; multimatrix.py:97-158)
+// for one driver iteration.  One block of kPlanThreads: every slot's model,
+// status, rank and offset are loaded in parallel, the prefix sums (kept
+// widths, move lengths, retirement order) are block scans, and only the FIFO
+// admission with head-of-line blocking runs on one thread.
+__global__ void __launch_bounds__(kPlanThreads, 1) engine_plan_kernel(EngState* st) {
   if (st->done) return;
-  const int lane = threadIdx.x;
+  __shared__ int wtot[32];
+  __shared__ int s_new_w, s_new_n, s_retired, s_moves, s_pre;
   const unsigned long long now = globaltimer_ns();
   const int n_old = st->n_active;
-  int new_n = 0, new_w = 0, retired = st->n_retired, moves = 0, pre = 0;
-  for (int base = 0; base < n_old; base += 32) {
-    const int s = base + lane;
+  if (threadIdx.x == 0) {
+    s_new_w = 0;
+    s_new_n = 0;
+    s_retired = st->n_retired;
+    s_moves = 0;
+    s_pre = 0;
+  }
+  __syncthreads();
+  for (int base = 0; base < n_old; base += kPlanThreads) {
+    const int s = base + threadIdx.x;
     const bool valid = s < n_old;
     const int k = valid ? st->slot_model[s] : 0;
+    const int src = valid ? st->slot_off[s] : 0;
+    const int rank_k = valid ? st->rank[k] : 0;
     const bool retiring = valid && st->status[k] != kActive;
     const bool keep = valid && !retiring;
-    const int rk = keep ? st->rank[k] : 0;
-    int incl = rk;
-    for (int o = 1; o < 32; o <<= 1) {
-      const int v = __shfl_up_sync(0xffffffffu, incl, o);
-      if (lane >= o) incl += v;
-    }
-    const unsigned rmask = __ballot_sync(0xffffffffu, retiring);
-    const unsigned kmask = __ballot_sync(0xffffffffu, keep);
-    const unsigned below = (1u << lane) - 1u;
-    const int src = valid ? st->slot_off[s] : 0;
+    const int new_w = s_new_w, new_n = s_new_n, retired = s_retired, moves = s_moves,
+              pre = s_pre;
+    __syncthreads();  // everyone has read the carries (and its slot, compacted below)
+    const int rk = keep ? rank_k : 0;
+    int tw, tk, tr, tm;
+    const int incl = plan_scan(rk, wtot, &tw);
+    const int kidx = plan_scan(keep ? 1 : 0, wtot, &tk) - (keep ? 1 : 0);
+    const int ridx = plan_scan(retiring ? 1 : 0, wtot, &tr) - (retiring ? 1 : 0);
     const int dst_keep = new_w + incl - rk;
-    const int ml = retiring ? st->rank[k] : (keep && dst_keep != src ? rk : 0);
-    int mincl = ml;
-    for (int o = 1; o < 32; o <<= 1) {
-      const int v = __shfl_up_sync(0xffffffffu, mincl, o);
-      if (lane >= o) mincl += v;
-    }
-    if (retiring || keep) st->mv_pre[moves + __popc((rmask | kmask) & below)] = pre + mincl - ml;
-    if (retiring) {
-      const int seq = retired + __popc(rmask & below);
-      st->retire_seq[k] = seq;
-      st->t_retire[k] = now;
-      const int mi = moves + __popc((rmask | kmask) & below);
-      st->mv_kind[mi] = kMoveRetire;
+    const int ml = retiring ? rank_k : (keep && dst_keep != src ? rk : 0);
+    const int mincl = plan_scan(ml, wtot, &tm);
+    if (valid) {
+      const int mi = moves + (s - base);  // every valid slot is retiring or kept
+      st->mv_pre[mi] = pre + mincl - ml;
       st->mv_model[mi] = k;
       st->mv_src[mi] = src;
-      st->mv_dst[mi] = 0;
-      st->mv_len[mi] = st->rank[k];
+      if (retiring) {
+        st->retire_seq[k] = retired + ridx;
+        st->t_retire[k] = now;
+        st->mv_kind[mi] = kMoveRetire;
+        st->mv_dst[mi] = 0;
+        st->mv_len[mi] = rank_k;
+      } else {
+        st->mv_kind[mi] = kMoveKeep;
+        st->mv_dst[mi] = dst_keep;
+        st->mv_len[mi] = dst_keep != src ? rk : 0;
+        // slot arrays are compacted in place: new index <= s, and every slot
+        // of this chunk was read before the barrier above
+        st->slot_model[new_n + kidx] = k;
+        st->slot_off[new_n + kidx] = dst_keep;
+      }
     }
-    if (keep) {
-      const int dst = new_w + incl - rk;
-      const int ns = new_n + __popc(kmask & below);
-      // slot arrays are compacted in place: ns <= s and every read of slot s
-      // in this warp happened above
-      const int mi = moves + __popc((rmask | kmask) & below);
-      st->mv_kind[mi] = kMoveKeep;
-      st->mv_model[mi] = k;
-      st->mv_src[mi] = src;
-      st->mv_dst[mi] = dst;
-      st->mv_len[mi] = dst != src ? rk : 0;
-      __syncwarp(kmask);
-      st->slot_model[ns] = k;
-      st->slot_off[ns] = dst;
+    if (threadIdx.x == 0) {
+      s_new_w = new_w + tw;
+      s_new_n = new_n + tk;
+      s_retired = retired + tr;
+      s_moves = moves + min(kPlanThreads, n_old - base);
+      s_pre = pre + tm;
     }
-    __syncwarp();
-    new_w += __shfl_sync(0xffffffffu, incl, 31);
-    new_n += __popc(kmask);
-    retired += __popc(rmask);
-    moves += __popc(rmask | kmask);
-    pre += __shfl_sync(0xffffffffu, mincl, 31);
+    __syncthreads();
   }
-  if (lane == 0) {
+  if (threadIdx.x == 0) {
+    int new_w = s_new_w, new_n = s_new_n, moves = s_moves, pre = s_pre;
     int head = st->queue_head;
     while (head < st->n_models && new_w + st->rank[head] <= st->capacity) {
       const int k = head++;
@@ -512,7 +546,7 @@ __global__ void engine_plan_kernel(EngState* st) {
     st->queue_head = head;
     st->n_active = new_n;
     st->width = new_w;
-    st->n_retired = retired;
+    st->n_retired = s_retired;
     const int rec = st->plans_done;
     if (rec < st->tr_cap) {
       st->tr_width[rec] = new_w;
@@ -995,7 +1029,7 @@ static int enqueue_mode_update(Engine* e, int n, cudaStream_t stream) {
 }
 
 static int enqueue_plan(Engine* e, cudaStream_t stream) {
-  engine_plan_kernel<<<1, 32, 0, stream>>>(e->d_st);
+  engine_plan_kernel<<<1, kPlanThreads, 0, stream>>>(e->d_st);
   CALS_CUDA_TRY(cudaGetLastError());
   engine_move_kernel<<<e->move_grid, 256, e->move_smem, stream>>>(e->d_st);
   CALS_CUDA_TRY(cudaGetLastError());
@@ -1166,7 +1200,7 @@ static int engine_run(Engine* e, double tol, int max_iterations, double sqnorm, 
   rc = engine_prepare_slices(e, stream);
   if (rc) return rc;
   // initial admission
-  engine_plan_kernel<<<1, 32, 0, stream>>>(e->d_st);
+  engine_plan_kernel<<<1, kPlanThreads, 0, stream>>>(e->d_st);
   engine_move_kernel<<<e->move_grid, 256, e->move_smem, stream>>>(e->d_st);
   CALS_CUDA_TRY(cudaGetLastError());
   if (use_graph) {
