@@ -343,12 +343,12 @@ int launch_contraction_ozaki(Tensor& t, const ModePlan& p, int key, const double
   a.tm_full = mt.tm_full;
   a.rem_rows = mt.rem_rows;
   a.rem_slabs = mt.rem_slabs;
-  static const int dbg = getenv("CALS_OZ_DBG") ? atoi(getenv("CALS_OZ_DBG")) : 0;
-  a.dbg = dbg;
+#ifdef CALS_OZ_PROFILE
+  // profiling builds: per-CTA cycle counters of the previous launch on stderr
   static unsigned long long* prof = nullptr;
-  if ((dbg & 8) && !prof) cudaMalloc(&prof, 148 * 12 * 8);
+  if (!prof) cudaMalloc(&prof, 148 * 12 * 8);
   a.prof = prof;
-  if (dbg & 8) {
+  {
     static int calls = 0;
     if (calls++ > 0) {
       unsigned long long h[148 * 12];
@@ -367,6 +367,9 @@ int launch_contraction_ozaki(Tensor& t, const ModePlan& p, int key, const double
               mx, sf, st, ns);
     }
   }
+#else
+  a.prof = nullptr;
+#endif
 
   static std::once_flag attr_once;
   static cudaError_t attr_err = cudaSuccess;

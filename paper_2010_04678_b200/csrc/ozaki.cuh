@@ -64,6 +64,12 @@ constexpr int kTmemCols = 512;
 // overwrites the buffer of this slab's group g - 1 (drained one group
 // earlier) -- one group of slack between the epilogue and the MMA warp.
 constexpr int kTmemBufs = 8;
+#ifdef CALS_OZ_PROFILE
+constexpr bool kProfile = true;
+#else
+constexpr bool kProfile = false;
+#endif
+__device__ __forceinline__ long long prof_clock() { return kProfile ? clock64() : 0; }
 // cross-slab FP64 accumulator of the epilogue: [32 rows m][256 epilogue threads]
 constexpr size_t kAccBytes = size_t(32) * 32 * kEpiWarps * 8;
 constexpr size_t kSmemBytes =
@@ -93,8 +99,9 @@ struct Args {
   int tm_full;
   int rem_rows;
   int rem_slabs;
-  int dbg;           // timing experiments only: 1 = no TMA, 2 = no epilogue math
-  unsigned long long* prof;  // dbg & 8: per-CTA {total, wait_full, wait_tempty} cycles
+  // CALS_OZ_PROFILE builds only: per-CTA cycle counters (MMA waits, epilogue
+  // phases) -- see tools/oz_time.py
+  unsigned long long* prof;
 };
 
 // ------------------------------------------------------------ instruction --
@@ -176,17 +183,17 @@ __device__ __forceinline__ void drain_pass(uint64_t* tfull, uint64_t* tempty, ui
   long long Qv[32];
 #pragma unroll
   for (int g = 0; g < kGroups; ++g) {
-    const long long e0 = clock64();
+    const long long e0 = prof_clock();
     const uint32_t L = 7u * slab + g, buf = L & 7u;
     mbar_wait(&tfull[buf], (L >> 3) & 1u);
     tc_fence_after();
-    const long long e1 = clock64();
+    const long long e1 = prof_clock();
     ew_wait += e1 - e0;
     tmem_ld32(trow + buf * BNM, v);
     tc_fence_before();
     __syncwarp();
     if (lane == 0) mbar_arrive(&tempty[buf]);  // TMEM buffer free for its next use
-    ew_load += clock64() - e1;
+    ew_load += prof_clock() - e1;
     if (g == 0) {
 #pragma unroll
       for (int j = 0; j < 32; ++j) Qv[j] = (long long)(int)v[j];
@@ -268,11 +275,6 @@ __global__ void __launch_bounds__(kThreads, 1)
           for (int ks = 0; ks < KS; ++ks) {
             mbar_wait(&empty[stage], phase ^ 1u);
             unsigned char* st = smem + size_t(stage) * kStageBytes;
-            if ((args.dbg & 1) && (i > 1)) {
-              mbar_arrive(&full[stage]);
-              if (++stage == STAGES) { stage = 0; phase ^= 1u; }
-              continue;
-            }
             if (U.rem) {
               // rows M-r..M-1 of slabs qb.. (rem_slabs of them), one box per
               // slice at the slice's 2048-byte B-tile offset
@@ -302,16 +304,16 @@ __global__ void __launch_bounds__(kThreads, 1)
     uint32_t slab = 0;
     const uint64_t sdesc = desc_sw32(smem_u32(smem));
     long long w_full = 0, w_tempty = 0;
-    const long long t_start = clock64();
+    const long long t_start = prof_clock();
     for (int u = blockIdx.x; u < units; u += gridDim.x) {
       const Unit U = unit_decode(u, tn, args);
       const int passes = U.rem ? 1 : U.qe - U.qb;
       for (int i = 0; i < passes; ++i, ++slab) {
         for (int ks = 0; ks < KS; ++ks) {
-          long long t0 = clock64();
+          long long t0 = prof_clock();
           mbar_wait(&full[stage], phase);
           tc_fence_after();
-          w_full += clock64() - t0;
+          w_full += prof_clock() - t0;
           // descriptor start-address field counts 16-byte units
           const uint64_t a0 = sdesc + (uint64_t)((stage * kStageBytes) >> 4);
           const uint64_t b0 = a0 + (uint64_t)(kLoStageBytes >> 4);
@@ -331,10 +333,10 @@ __global__ void __launch_bounds__(kThreads, 1)
               const uint32_t buf = (L0 + g) & 7u, use = (L0 + g) >> 3;
               if (ks == 0) {
                 // the epilogue must have drained this buffer's previous use
-                long long t1 = clock64();
+                long long t1 = prof_clock();
                 mbar_wait(&tempty[buf], (use & 1u) ^ 1u);
                 tc_fence_after();
-                w_tempty += clock64() - t1;
+                w_tempty += prof_clock() - t1;
               }
 #pragma unroll
               for (int i = i_lo; i <= i_hi; ++i) {
@@ -351,8 +353,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
       }
     }
-    if ((args.dbg & 8) && lane == 0) {
-      args.prof[blockIdx.x * 4 + 0] = clock64() - t_start;
+    if (kProfile && lane == 0) {
+      args.prof[blockIdx.x * 4 + 0] = prof_clock() - t_start;
       args.prof[blockIdx.x * 4 + 1] = w_full;
       args.prof[blockIdx.x * 4 + 2] = w_tempty;
       args.prof[blockIdx.x * 4 + 3] = slab;
@@ -373,7 +375,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     const uint32_t trow = tmem + ((uint32_t)(quad * 32) << 16) + half * 32;
     uint32_t slab = 0;
     long long ew_wait = 0, ew_load = 0, ew_final = 0;
-    const long long e_start = clock64();
+    const long long e_start = prof_clock();
     for (int u = blockIdx.x; u < units; u += gridDim.x) {
       const Unit U = unit_decode(u, tn, args);
       const int c = U.tc * BMC + quad * 32 + lane;
@@ -402,7 +404,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           const int rex_lane =
               mb + lane < args.M ? __ldg(args.rex + (long long)q * args.M + mb + lane) : 0;
           drain_pass(tfull, tempty, slab, trow, lane, P, ew_wait, ew_load);
-          const long long e2 = clock64();
+          const long long e2 = prof_clock();
           // Scaling by 2^ex (row) and 2^(ex + el - 50) (side output) is an
           // exponent-field add on the integer pipe: P is the double of an
           // integer (0, or |P| in [1, 2^62)), row exponents are confined to
@@ -430,7 +432,7 @@ __global__ void __launch_bounds__(kThreads, 1)
               acc[j * 32 * kEpiWarps] = fma(y, hc, acc[j * 32 * kEpiWarps]);
             }
           }
-          ew_final += clock64() - e2;
+          ew_final += prof_clock() - e2;
         }
         if (cval) {
           double* out = args.out + (args.S > 1 ? (long long)U.s * args.part_stride : 0LL);
@@ -478,10 +480,10 @@ __global__ void __launch_bounds__(kThreads, 1)
         asm volatile("bar.sync %0, 64;" ::"r"(1 + quad) : "memory");
       }
     }
-    if ((args.dbg & 8) && lane == 0 && (warp == 2 || warp == 5)) {
+    if (kProfile && lane == 0 && (warp == 2 || warp == 5)) {
       // epilogue timing (warp 2: SMSP 2; warp 5: shares SMSP 1 with the MMA warp)
       unsigned long long* p = args.prof + 148 * 4 + (blockIdx.x * 2 + (warp == 5)) * 4;
-      p[0] = clock64() - e_start;
+      p[0] = prof_clock() - e_start;
       p[1] = ew_wait;
       p[2] = ew_load;
       p[3] = ew_final;
