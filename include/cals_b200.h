@@ -96,6 +96,10 @@ int cals_engine_destroy(cals_engine* e);
 /* Re-bind an engine (and its device workspaces) to another tensor of the same
  * shape, so repeated sweeps reuse every allocation. */
 int cals_engine_set_tensor(cals_engine* e, cals_tensor* t);
+/* Enqueue the once-per-tensor preparation of the engine's INT8 tensor-core
+ * views (tensor slicing) on `stream` without waiting: lets it overlap host
+ * work before cals_engine_run (which finishes and checks it). */
+int cals_engine_prepare(cals_engine* e, void* stream);
 int cals_engine_pool(cals_engine* e, double** pool, int64_t* elems);
 int cals_engine_load_pool(cals_engine* e, const double* src, int src_is_device, void* stream);
 /* Runs until every model has retired (ConvergenceConfig semantics,

@@ -43,6 +43,7 @@ SIGNATURES = {
     "cals_engine_create": (C.c_int, [C.c_void_p, C.c_int, C.c_int, C.POINTER(C.c_int32), C.c_int,
                                      c_void_pp]),
     "cals_engine_destroy": (C.c_int, [C.c_void_p]),
+    "cals_engine_prepare": (C.c_int, [C.c_void_p, C.c_void_p]),
     "cals_engine_set_tensor": (C.c_int, [C.c_void_p, C.c_void_p]),
     "cals_engine_pool": (C.c_int, [C.c_void_p, c_void_pp, c_i64_p]),
     "cals_engine_load_pool": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int, C.c_void_p]),

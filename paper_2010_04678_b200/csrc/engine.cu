@@ -720,17 +720,17 @@ static size_t tree_ws_offset(const ModePlan& p, long long ld) {
 
 // Ozaki X slices for every view this engine contracts (built once per tensor,
 // before any graph capture).
-static int engine_prepare_slices(Engine* e, cudaStream_t stream) {
+static int engine_prepare_slices(Engine* e, cudaStream_t stream, bool validate = true) {
   Tensor& t = *e->t;
   const int N = e->order;
   for (int n = 0; n < N; ++n) {
     const bool used = e->tree == kTreeNone || n == N - 1 || (e->tree == kTreeZ && n == 0);
     if (!used) continue;
-    const int rc = ozaki_prepare(t, t.plans[n], n, stream);
+    const int rc = ozaki_prepare(t, t.plans[n], n, stream, validate);
     if (rc) return rc;
   }
-  if (e->tree == kTreeY) return ozaki_prepare(t, e->tree_plan, 100, stream);
-  if (e->tree == kTreeZ) return ozaki_prepare(t, e->tree_plan, 1, stream);
+  if (e->tree == kTreeY) return ozaki_prepare(t, e->tree_plan, 100, stream, validate);
+  if (e->tree == kTreeZ) return ozaki_prepare(t, e->tree_plan, 1, stream, validate);
   return kOk;
 }
 
@@ -1491,6 +1491,11 @@ int cals_nnls_rows(int rows, int rank, const double* m, int64_t ldm, const doubl
       rows, rank, m, ldm, h, active, x, ldx, converged, max_iter);
   CALS_CUDA_TRY(cudaGetLastError());
   return kOk;
+}
+
+int cals_engine_prepare(cals_engine* e, void* stream) {
+  CALS_CHECK(e, kErrInvalid, "null engine");
+  return engine_prepare_slices(e->e, (cudaStream_t)stream, false);
 }
 
 int cals_engine_set_nonneg(cals_engine* e, int enabled) {

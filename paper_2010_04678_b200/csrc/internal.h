@@ -37,6 +37,7 @@ struct ModePlan {
 struct OzSlices {
   uint8_t* xs = nullptr;
   int* rex = nullptr;
+  int* flag = nullptr;  // device flag of a slicing not yet checked (ozaki_validate)
   long long Kp = 0, M = 0, Dq = 0, Dp = 0;
   CUtensorMap map;   // full 64-row tiles
   CUtensorMap rmap;  // packed remainder tiles (== map when unused)
@@ -112,7 +113,11 @@ bool ozaki_eligible(const ModePlan& p);
 size_t ozaki_ws_bytes(const ModePlan& p, long long cap);  // per-call Lo slices
 double ozaki_tensor_ops(const ModePlan& p, long long width);  // INT8 ops per launch
 // Build (once per tensor and key) the X slices of view `p`; stream-ordered.
-int ozaki_prepare(Tensor& t, const ModePlan& p, int key, cudaStream_t stream);
+// validate = false defers the range / finiteness check (one host sync) to
+// ozaki_validate; unchecked slices are not used by launches.
+int ozaki_prepare(Tensor& t, const ModePlan& p, int key, cudaStream_t stream,
+                  bool validate = true);
+int ozaki_validate(Tensor& t, int key, cudaStream_t stream);
 void ozaki_release(Tensor& t);
 int launch_contraction_ozaki(Tensor& t, const ModePlan& p, int key, const double* lo,
                              long long lrows, long long lo_ld, const double* hi, long long hi_ld,

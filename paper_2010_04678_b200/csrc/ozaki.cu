@@ -209,11 +209,45 @@ size_t ozaki_ws_bytes(const ModePlan& p, long long cap) {
   return size_t(kSlices) * size_t(cap_pad) * size_t(kp_of(p.Dp)) + size_t(cap_pad) * 8 + 1024;
 }
 
-int ozaki_prepare(Tensor& t, const ModePlan& p, int key, cudaStream_t stream) {
+// A view whose slicing found rows beyond 2^+-900 or a non-finite entry is
+// dropped (it stays on DMMA).  The check reads a device flag: done here when
+// `validate`, else deferred to ozaki_validate (so the slicing can overlap
+// host work, e.g. the pool packing of run()).
+static int ozaki_check(Tensor& t, int key, OzSlices& o, cudaStream_t stream, bool* keep) {
+  int h_flag = 0;
+  CALS_CUDA_TRY(cudaMemcpyAsync(&h_flag, o.flag, sizeof(int), cudaMemcpyDeviceToHost, stream));
+  CALS_CUDA_TRY(cudaStreamSynchronize(stream));
+  CALS_CUDA_TRY(cudaFreeAsync(o.flag, stream));
+  o.flag = nullptr;
+  *keep = h_flag == 0;
+  if (!*keep) {
+    cudaFreeAsync(o.xs, stream);
+    cudaFreeAsync(o.rex, stream);
+  }
+  (void)t;
+  (void)key;
+  return kOk;
+}
+
+int ozaki_validate(Tensor& t, int key, cudaStream_t stream) {
+  std::lock_guard<std::mutex> lk(t.mu);
+  auto it = t.oz.find(key);
+  if (it == t.oz.end() || !it->second.flag) return kOk;
+  bool keep = true;
+  const int rc = ozaki_check(t, key, it->second, stream, &keep);
+  if (rc) return rc;
+  if (!keep) t.oz.erase(it);
+  return kOk;
+}
+
+int ozaki_prepare(Tensor& t, const ModePlan& p, int key, cudaStream_t stream, bool validate) {
   if (!ozaki_eligible(p)) return kOk;
   {
-    std::lock_guard<std::mutex> lk(t.mu);
-    if (t.oz.count(key)) return kOk;
+    std::unique_lock<std::mutex> lk(t.mu);
+    if (t.oz.count(key)) {
+      lk.unlock();
+      return validate ? ozaki_validate(t, key, stream) : kOk;
+    }
   }
   long long sm, sp, sq;
   if (view_strides(t, p, sm, sp, sq)) return kOk;
@@ -240,16 +274,11 @@ int ozaki_prepare(Tensor& t, const ModePlan& p, int key, cudaStream_t stream) {
   oz_slice_rows_kernel<<<grid, 256, 0, stream>>>(t.data, sm, sp, sq, (int)p.M, (int)p.Dp,
                                                  (int)o.Kp, (int)p.Dq, o.xs, o.rex, flag);
   CALS_CUDA_TRY(cudaGetLastError());
-  // once per tensor and view: a tensor with rows beyond 2^+-900 or with a
-  // non-finite entry stays on DMMA
-  int h_flag = 0;
-  CALS_CUDA_TRY(cudaMemcpyAsync(&h_flag, flag, sizeof(int), cudaMemcpyDeviceToHost, stream));
-  CALS_CUDA_TRY(cudaStreamSynchronize(stream));
-  CALS_CUDA_TRY(cudaFreeAsync(flag, stream));
-  if (h_flag) {
-    cudaFreeAsync(o.xs, stream);
-    cudaFreeAsync(o.rex, stream);
-    return kOk;
+  o.flag = flag;
+  if (validate) {  // once per tensor and view
+    bool keep = true;
+    const int rc = ozaki_check(t, key, o, stream, &keep);
+    if (rc || !keep) return rc;
   }
   {
     const uint64_t dims[4] = {(uint64_t)o.Kp, (uint64_t)p.M, (uint64_t)p.Dq, (uint64_t)kSlices};
@@ -271,6 +300,7 @@ int ozaki_prepare(Tensor& t, const ModePlan& p, int key, cudaStream_t stream) {
   if (t.oz.count(key)) {  // another thread raced us: keep theirs
     cudaFreeAsync(o.xs, stream);
     cudaFreeAsync(o.rex, stream);
+    if (o.flag) cudaFreeAsync(o.flag, stream);
     return kOk;
   }
   t.oz.emplace(key, o);
@@ -281,6 +311,7 @@ void ozaki_release(Tensor& t) {
   for (auto& kv : t.oz) {
     cudaFreeAsync(kv.second.xs, 0);
     cudaFreeAsync(kv.second.rex, 0);
+    if (kv.second.flag) cudaFreeAsync(kv.second.flag, 0);
   }
   t.oz.clear();
 }
@@ -295,7 +326,7 @@ int launch_contraction_ozaki(Tensor& t, const ModePlan& p, int key, const double
   {
     std::lock_guard<std::mutex> lk(t.mu);
     auto it = t.oz.find(key);
-    if (it == t.oz.end()) return kErrUnsupported;
+    if (it == t.oz.end() || it->second.flag) return kErrUnsupported;  // absent / unchecked
     o = it->second;
   }
   CALS_CHECK(o.M == p.M && o.Dq == p.Dq && o.Dp == p.Dp, kErrInvalid, "Ozaki slices / plan mismatch");

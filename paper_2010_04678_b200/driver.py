@@ -154,6 +154,7 @@ def _run_fused(t: DenseTensor, queue: list[Model], cfg: ConvergenceConfig, r_sta
     eng = _ENGINES.acquire(dev, r_star, ranks, tcap)
     t2 = time.perf_counter()
     try:
+        eng.prepare()  # tensor slicing overlaps the host packing below
         eng.set_line_search(bool(ls is not None and ls.enabled), None if ls is None else ls.alpha)
         eng.set_nonneg(nonneg)
         eng.load_pool(eng.pack([m.factors for m in queue], out=eng.staging()))

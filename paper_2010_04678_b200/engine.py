@@ -77,6 +77,14 @@ class CalsEngine:
             self._staging = self._staging_t.numpy()
         return self._staging
 
+    def prepare(self, stream=None):
+        """Enqueue the tensor slicing of the INT8 tensor-core views without
+        waiting (finished and checked by ``run``)."""
+        import torch
+
+        s = stream if stream is not None else torch.cuda.current_stream().cuda_stream
+        _native.call("cals_engine_prepare", self.handle, s)
+
     def set_tensor(self, dev_tensor):
         """Re-bind to another device tensor of the same shape."""
         _native.call("cals_engine_set_tensor", self.handle, dev_tensor.handle)
