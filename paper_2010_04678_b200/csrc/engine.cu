@@ -671,6 +671,8 @@ struct Engine {
   size_t ws_bytes = 0;
   double* d_ws = nullptr;
   int* h_done = nullptr;  // mapped pinned
+  char* h_results = nullptr;  // pinned staging of the per-model results
+  size_t h_results_bytes = 0;
   int* d_done_alias = nullptr;
   int variants[kMaxOrder];
   // dimension tree (order 3): share one tensor-core contraction between two modes
@@ -788,6 +790,7 @@ static int engine_free(Engine* e) {
   if (e->d_nnls) cudaFree(e->d_nnls);
   if (e->d_st) cudaFree(e->d_st);
   if (e->h_done) cudaFreeHost(e->h_done);
+  if (e->h_results) cudaFreeHost(e->h_results);
   delete e;
   return kOk;
 }
@@ -1406,28 +1409,52 @@ int cals_engine_results(cals_engine* e, double* pool, int32_t* status, int32_t* 
   const size_t nm = size_t(g->n_models);
   if (nm == 0) return kOk;
   const EngState& h = g->h_st;
+  // the small per-model arrays land in one page-locked block (async copies
+  // are cheap there; pageable ones each cost a synchronous round trip), then
+  // one host copy each into the caller's arrays
+  const size_t lam_bytes = size_t(g->lam_elems) * 8;
+  const size_t need = nm * (4 + 4 + 8 + 8 + 4 + 8 + 8) + lam_bytes + 64;
+  if (g->h_results_bytes < need) {
+    if (g->h_results) cudaFreeHost(g->h_results);
+    g->h_results = nullptr;
+    g->h_results_bytes = 0;
+    CALS_CUDA_TRY(cudaHostAlloc(reinterpret_cast<void**>(&g->h_results), need, 0));
+    g->h_results_bytes = need;
+  }
+  char* hb = g->h_results;
+  int32_t* hs = reinterpret_cast<int32_t*>(hb);
+  int32_t* hi = hs + nm;
+  int32_t* hq = hi + nm;
+  double* he = reinterpret_cast<double*>(hb + ((nm * 12 + 7) / 8) * 8);
+  double* hf = he + nm;
+  unsigned long long* ta = reinterpret_cast<unsigned long long*>(hf + nm);
+  unsigned long long* tr = ta + nm;
+  double* hl = reinterpret_cast<double*>(tr + nm);
   if (lambdas) {
     lambdas_kernel<<<std::min<int>(g->n_models, 1024), 32, 0, s>>>(g->d_st, g->d_lam_off,
                                                                  g->d_lam);
     CALS_CUDA_TRY(cudaGetLastError());
-    CALS_CUDA_TRY(cudaMemcpyAsync(lambdas, g->d_lam, size_t(g->lam_elems) * 8,
-                                  cudaMemcpyDeviceToHost, s));
+    CALS_CUDA_TRY(cudaMemcpyAsync(hl, g->d_lam, lam_bytes, cudaMemcpyDeviceToHost, s));
   }
   if (pool)
     CALS_CUDA_TRY(cudaMemcpyAsync(pool, h.pool, size_t(g->pool_elems) * 8, cudaMemcpyDeviceToHost, s));
-  if (status) CALS_CUDA_TRY(cudaMemcpyAsync(status, h.status, nm * 4, cudaMemcpyDeviceToHost, s));
-  if (iterations)
-    CALS_CUDA_TRY(cudaMemcpyAsync(iterations, h.iters, nm * 4, cudaMemcpyDeviceToHost, s));
-  if (error) CALS_CUDA_TRY(cudaMemcpyAsync(error, h.err, nm * 8, cudaMemcpyDeviceToHost, s));
-  if (fit) CALS_CUDA_TRY(cudaMemcpyAsync(fit, h.fit, nm * 8, cudaMemcpyDeviceToHost, s));
+  if (status) CALS_CUDA_TRY(cudaMemcpyAsync(hs, h.status, nm * 4, cudaMemcpyDeviceToHost, s));
+  if (iterations) CALS_CUDA_TRY(cudaMemcpyAsync(hi, h.iters, nm * 4, cudaMemcpyDeviceToHost, s));
   if (retire_seq)
-    CALS_CUDA_TRY(cudaMemcpyAsync(retire_seq, h.retire_seq, nm * 4, cudaMemcpyDeviceToHost, s));
-  std::vector<unsigned long long> ta(nm), tr(nm);
+    CALS_CUDA_TRY(cudaMemcpyAsync(hq, h.retire_seq, nm * 4, cudaMemcpyDeviceToHost, s));
+  if (error) CALS_CUDA_TRY(cudaMemcpyAsync(he, h.err, nm * 8, cudaMemcpyDeviceToHost, s));
+  if (fit) CALS_CUDA_TRY(cudaMemcpyAsync(hf, h.fit, nm * 8, cudaMemcpyDeviceToHost, s));
   if (seconds_active) {
-    CALS_CUDA_TRY(cudaMemcpyAsync(ta.data(), h.t_admit, nm * 8, cudaMemcpyDeviceToHost, s));
-    CALS_CUDA_TRY(cudaMemcpyAsync(tr.data(), h.t_retire, nm * 8, cudaMemcpyDeviceToHost, s));
+    CALS_CUDA_TRY(cudaMemcpyAsync(ta, h.t_admit, nm * 8, cudaMemcpyDeviceToHost, s));
+    CALS_CUDA_TRY(cudaMemcpyAsync(tr, h.t_retire, nm * 8, cudaMemcpyDeviceToHost, s));
   }
   CALS_CUDA_TRY(cudaStreamSynchronize(s));
+  if (status) memcpy(status, hs, nm * 4);
+  if (iterations) memcpy(iterations, hi, nm * 4);
+  if (retire_seq) memcpy(retire_seq, hq, nm * 4);
+  if (error) memcpy(error, he, nm * 8);
+  if (fit) memcpy(fit, hf, nm * 8);
+  if (lambdas) memcpy(lambdas, hl, lam_bytes);
   if (seconds_active)
     for (size_t k = 0; k < nm; ++k) seconds_active[k] = (double)(tr[k] - ta[k]) * 1e-9;
   return kOk;
