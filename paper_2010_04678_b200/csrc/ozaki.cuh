@@ -319,12 +319,30 @@ __global__ void __launch_bounds__(kThreads, 1)
           const uint64_t b0 = a0 + (uint64_t)(kLoStageBytes >> 4);
           // group g of this slab -> buffer (7 slab + g) mod 8, use (7 slab + g) / 8
           const uint32_t L0 = 7u * slab;
-          if (ks > 0 && ks < KS - 1) {
+          if (ks > 0) {
             uint32_t d[7];
 #pragma unroll
             for (int g = 0; g < kGroups; ++g) d[g] = tmem + ((L0 + g) & 7u) * BNM;
-            issue_kstep(d, a0, b0, 0u);
+            if (ks < KS - 1) {
+              issue_kstep(d, a0, b0, 0u);
+            } else {
+              uint32_t bar[7];
+#pragma unroll
+              for (int g = 0; g < kGroups; ++g) bar[g] = smem_u32(&tfull[(L0 + g) & 7u]);
+              issue_kstep_last(d, a0, b0, bar);
+            }
+          } else if (KS > 1) {
+            uint32_t d[7], bar[7], par[7];
+#pragma unroll
+            for (int g = 0; g < kGroups; ++g) {
+              const uint32_t buf = (L0 + g) & 7u, use = (L0 + g) >> 3;
+              d[g] = tmem + buf * BNM;
+              bar[g] = smem_u32(&tempty[buf]);
+              par[g] = (use & 1u) ^ 1u;
+            }
+            issue_kstep_first(d, a0, b0, bar, par);
           } else {
+            // a single K step: first and last at once (per-group waits and commits)
 #pragma unroll
             for (int g = 0; g < kGroups; ++g) {
               const int sum = g + 2;
