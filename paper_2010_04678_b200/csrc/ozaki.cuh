@@ -309,34 +309,37 @@ __global__ void __launch_bounds__(kThreads, 1)
       const Unit U = unit_decode(u, tn, args);
       const int passes = U.rem ? 1 : U.qe - U.qb;
       for (int i = 0; i < passes; ++i, ++slab) {
+        // group g of this slab -> buffer (7 slab + g) mod 8, use (7 slab + g) / 8
+        const uint32_t L0 = 7u * slab;
+        uint32_t d[7];
+#pragma unroll
+        for (int g = 0; g < kGroups; ++g) d[g] = tmem + ((L0 + g) & 7u) * BNM;
         for (int ks = 0; ks < KS; ++ks) {
+          // descriptor start-address field counts 16-byte units
+          const uint64_t a0 = sdesc + (uint64_t)((stage * kStageBytes) >> 4);
+          const uint64_t b0 = a0 + (uint64_t)(kLoStageBytes >> 4);
+          if (ks > 0 && ks < KS - 1) {
+            // interior K step: wait, 28 products, release -- one asm block
+            issue_kstep_mid(d, a0, b0, smem_u32(&full[stage]), phase, smem_u32(&empty[stage]));
+            if (++stage == STAGES) { stage = 0; phase ^= 1u; }
+            continue;
+          }
           long long t0 = prof_clock();
           mbar_wait(&full[stage], phase);
           tc_fence_after();
           w_full += prof_clock() - t0;
-          // descriptor start-address field counts 16-byte units
-          const uint64_t a0 = sdesc + (uint64_t)((stage * kStageBytes) >> 4);
-          const uint64_t b0 = a0 + (uint64_t)(kLoStageBytes >> 4);
-          // group g of this slab -> buffer (7 slab + g) mod 8, use (7 slab + g) / 8
-          const uint32_t L0 = 7u * slab;
           if (ks > 0) {
-            uint32_t d[7];
-#pragma unroll
-            for (int g = 0; g < kGroups; ++g) d[g] = tmem + ((L0 + g) & 7u) * BNM;
-            if (ks < KS - 1) {
-              issue_kstep(d, a0, b0, 0u);
-            } else {
+            {
               uint32_t bar[7];
 #pragma unroll
               for (int g = 0; g < kGroups; ++g) bar[g] = smem_u32(&tfull[(L0 + g) & 7u]);
               issue_kstep_last(d, a0, b0, bar);
             }
           } else if (KS > 1) {
-            uint32_t d[7], bar[7], par[7];
+            uint32_t bar[7], par[7];
 #pragma unroll
             for (int g = 0; g < kGroups; ++g) {
               const uint32_t buf = (L0 + g) & 7u, use = (L0 + g) >> 3;
-              d[g] = tmem + buf * BNM;
               bar[g] = smem_u32(&tempty[buf]);
               par[g] = (use & 1u) ^ 1u;
             }

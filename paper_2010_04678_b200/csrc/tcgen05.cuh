@@ -197,6 +197,75 @@ __device__ __forceinline__ void issue_kstep_first(const uint32_t (&d)[7], uint64
       : "memory");
 }
 
+// An interior K step as one asm block: wait for the stage's operands (full
+// barrier, parity), the 28 accumulating products, release the stage (commit
+// to its empty barrier).
+__device__ __forceinline__ void issue_kstep_mid(const uint32_t (&d)[7], uint64_t a0, uint64_t b0,
+                                                uint32_t full_bar, uint32_t full_parity,
+                                                uint32_t empty_bar) {
+  asm volatile(
+      "{\n"
+      ".reg .pred e, pw, pt;\n"
+      ".reg .b64 a<8>, b<8>;\n"
+      ".reg .b32 iss, isu, ius, iuu;\n"
+      "setp.eq.u32 pt, %0, %0;\n"
+      "mov.b64 a1, %7;\n"
+      "mov.b64 b1, %8;\n"
+      "add.s64 a2, %7, 256;\n"
+      "add.s64 b2, %8, 128;\n"
+      "add.s64 a3, %7, 512;\n"
+      "add.s64 b3, %8, 256;\n"
+      "add.s64 a4, %7, 768;\n"
+      "add.s64 b4, %8, 384;\n"
+      "add.s64 a5, %7, 1024;\n"
+      "add.s64 b5, %8, 512;\n"
+      "add.s64 a6, %7, 1280;\n"
+      "add.s64 b6, %8, 640;\n"
+      "add.s64 a7, %7, 1536;\n"
+      "add.s64 b7, %8, 768;\n"
+      "mov.b32 iss, 135267488;\n"
+      "mov.b32 isu, 135266464;\n"
+      "mov.b32 ius, 135267360;\n"
+      "mov.b32 iuu, 135266336;\n"
+      "WF_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 pw, [%9], %10;\n"
+      "@!pw bra WF_%=;\n"
+      "tcgen05.fence::after_thread_sync;\n"
+      "elect.sync _|e, 0xffffffff;\n"
+      "@e tcgen05.mma.cta_group::1.kind::i8 [%0], a1, b1, iss, pt;\n"
+      "@e tcgen05.mma.cta_group::1.kind::i8 [%1], a1, b2, isu, pt;\n"
+      "@e tcgen05.mma.cta_group::1.kind::i8 [%1], a2, b1, ius, pt;\n"
+      "@e tcgen05.mma.cta_group::1.kind::i8 [%2], a1, b3, isu, pt;\n"
+      "@e tcgen05.mma.cta_group::1.kind::i8 [%2], a2, b2, iuu, pt;\n"
+      "@e tcgen05.mma.cta_group::1.kind::i8 [%2], a3, b1, ius, pt;\n"
+      "@e tcgen05.mma.cta_group::1.kind::i8 [%3], a1, b4, isu, pt;\n"
+      "@e tcgen05.mma.cta_group::1.kind::i8 [%3], a2, b3, iuu, pt;\n"
+      "@e tcgen05.mma.cta_group::1.kind::i8 [%3], a3, b2, iuu, pt;\n"
+      "@e tcgen05.mma.cta_group::1.kind::i8 [%3], a4, b1, ius, pt;\n"
+      "@e tcgen05.mma.cta_group::1.kind::i8 [%4], a1, b5, isu, pt;\n"
+      "@e tcgen05.mma.cta_group::1.kind::i8 [%4], a2, b4, iuu, pt;\n"
+      "@e tcgen05.mma.cta_group::1.kind::i8 [%4], a3, b3, iuu, pt;\n"
+      "@e tcgen05.mma.cta_group::1.kind::i8 [%4], a4, b2, iuu, pt;\n"
+      "@e tcgen05.mma.cta_group::1.kind::i8 [%4], a5, b1, ius, pt;\n"
+      "@e tcgen05.mma.cta_group::1.kind::i8 [%5], a1, b6, isu, pt;\n"
+      "@e tcgen05.mma.cta_group::1.kind::i8 [%5], a2, b5, iuu, pt;\n"
+      "@e tcgen05.mma.cta_group::1.kind::i8 [%5], a3, b4, iuu, pt;\n"
+      "@e tcgen05.mma.cta_group::1.kind::i8 [%5], a4, b3, iuu, pt;\n"
+      "@e tcgen05.mma.cta_group::1.kind::i8 [%5], a5, b2, iuu, pt;\n"
+      "@e tcgen05.mma.cta_group::1.kind::i8 [%5], a6, b1, ius, pt;\n"
+      "@e tcgen05.mma.cta_group::1.kind::i8 [%6], a1, b7, isu, pt;\n"
+      "@e tcgen05.mma.cta_group::1.kind::i8 [%6], a2, b6, iuu, pt;\n"
+      "@e tcgen05.mma.cta_group::1.kind::i8 [%6], a3, b5, iuu, pt;\n"
+      "@e tcgen05.mma.cta_group::1.kind::i8 [%6], a4, b4, iuu, pt;\n"
+      "@e tcgen05.mma.cta_group::1.kind::i8 [%6], a5, b3, iuu, pt;\n"
+      "@e tcgen05.mma.cta_group::1.kind::i8 [%6], a6, b2, iuu, pt;\n"
+      "@e tcgen05.mma.cta_group::1.kind::i8 [%6], a7, b1, ius, pt;\n"
+      "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%11];\n"
+      "}\n" ::"r"(d[0]), "r"(d[1]), "r"(d[2]), "r"(d[3]), "r"(d[4]), "r"(d[5]), "r"(d[6]),
+      "l"(a0), "l"(b0), "r"(full_bar), "r"(full_parity), "r"(empty_bar)
+      : "memory");
+}
+
 // one elected lane of a converged warp issues (the operands are warp-uniform)
 __device__ __forceinline__ void mma_i8_elect(uint32_t d, uint64_t a, uint64_t b, uint32_t idesc,
                                              uint32_t acc) {
