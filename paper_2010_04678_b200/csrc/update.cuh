@@ -384,6 +384,62 @@ __device__ inline void block_gram_fast(const double* F, long long ld, int rows, 
   pr.store(G, R);
 }
 
+// One row's two triangular solves (U^T y = m, then U x = y; dpotrs order,
+// reciprocal diagonal) with the row in registers: the loops are unrolled to
+// the rank bucket RB (static register indices; steps beyond R are skipped by
+// a block-uniform branch), so each step is a chain of one multiply and the
+// independent FMAs of the remaining entries instead of shared-memory
+// read-modify-writes.  Same operation order as the shared-memory version.
+template <int RB>
+__device__ __forceinline__ void solve_row_reg(double* __restrict__ xs,
+                                              const double* __restrict__ U,
+                                              const double* __restrict__ inv_diag, int R) {
+  double x[RB];
+#pragma unroll
+  for (int a = 0; a < RB; ++a) x[a] = a < R ? xs[a] : 0.0;
+#pragma unroll
+  for (int k = 0; k < RB; ++k) {  // U^T y = m
+    if (k < R) {
+      const double yk = x[k] * inv_diag[k];
+      x[k] = yk;
+      const double* urow = U + k * R;
+#pragma unroll
+      for (int a = k + 1; a < RB; ++a)
+        if (a < R) x[a] = fma(-urow[a], yk, x[a]);
+    }
+  }
+#pragma unroll
+  for (int k = RB - 1; k >= 0; --k) {  // U x = y
+    if (k < R) {
+      const double xk = x[k] * inv_diag[k];
+      x[k] = xk;
+#pragma unroll
+      for (int a = 0; a < k; ++a) x[a] = fma(-U[a * R + k], xk, x[a]);
+    }
+  }
+#pragma unroll
+  for (int a = 0; a < RB; ++a)
+    if (a < R) xs[a] = x[a];
+}
+
+__device__ __forceinline__ void solve_row_smem(double* __restrict__ x,
+                                               const double* __restrict__ U,
+                                               const double* __restrict__ inv_diag, int R) {
+  for (int k = 0; k < R; ++k) {  // U^T y = m
+    const double xk = x[k] * inv_diag[k];
+    x[k] = xk;
+    const double* urow = U + k * R;
+#pragma unroll 4
+    for (int a = k + 1; a < R; ++a) x[a] = fma(-urow[a], xk, x[a]);
+  }
+  for (int k = R - 1; k >= 0; --k) {  // U x = y
+    const double xk = x[k] * inv_diag[k];
+    x[k] = xk;
+#pragma unroll 4
+    for (int a = 0; a < k; ++a) x[a] = fma(-U[a * R + k], xk, x[a]);
+  }
+}
+
 // Solve every row of the block against U (smem) / inv_diag, write A,
 // refresh G = A^T A and (want_inner) return sum(A o M).  Returns false when
 // a solution entry is non-finite (caller -> pinv path).  Rows go through Xs
@@ -410,19 +466,14 @@ __device__ __forceinline__ bool block_solve_gram_fast(const double* __restrict__
     }
     if (threadIdx.x < cnt) {
       double* x = Xs + threadIdx.x * P;
-      for (int k = 0; k < R; ++k) {  // U^T y = m
-        const double xk = x[k] * inv_diag[k];
-        x[k] = xk;
-        const double* urow = U + k * R;
-#pragma unroll 4
-        for (int a = k + 1; a < R; ++a) x[a] = fma(-urow[a], xk, x[a]);
-      }
-      for (int k = R - 1; k >= 0; --k) {  // U x = y
-        const double xk = x[k] * inv_diag[k];
-        x[k] = xk;
-#pragma unroll 4
-        for (int a = 0; a < k; ++a) x[a] = fma(-U[a * R + k], xk, x[a]);
-      }
+      if (R <= 8)
+        solve_row_reg<8>(x, U, inv_diag, R);
+      else if (R <= 16)
+        solve_row_reg<16>(x, U, inv_diag, R);
+      else if (R <= 24)
+        solve_row_reg<24>(x, U, inv_diag, R);
+      else  // 25..32: shared-memory rows (a 32-entry register row spills)
+        solve_row_smem(x, U, inv_diag, R);
     }
     __syncthreads();
     double* Ac = A + (long long)base * lda;
