@@ -405,14 +405,20 @@ int launch_contraction_ozaki(Tensor& t, const ModePlan& p, int key, const double
   static std::once_flag attr_once;
   static cudaError_t attr_err = cudaSuccess;
   std::call_once(attr_once, [] {
-    attr_err = cudaFuncSetAttribute(mttkrp_ozaki_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    (int)kSmemBytes);
+    attr_err = cudaFuncSetAttribute(mttkrp_ozaki_kernel<false>,
+                                    cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBytes);
+    if (attr_err == cudaSuccess)
+      attr_err = cudaFuncSetAttribute(mttkrp_ozaki_kernel<true>,
+                                      cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBytes);
   });
   CALS_CUDA_TRY(attr_err);
   const long long units =
       ((cap + BMC - 1) / BMC) * (mt.tm_full + (mt.rem_rows ? 1 : 0)) * (long long)p.S;
   dim3 grid((unsigned)std::max<long long>(1, std::min<long long>(units, sms)));
-  mttkrp_ozaki_kernel<<<grid, kThreads, kSmemBytes, stream>>>(o.map, mapL, o.rmap, a);
+  if (side)
+    mttkrp_ozaki_kernel<true><<<grid, kThreads, kSmemBytes, stream>>>(o.map, mapL, o.rmap, a);
+  else
+    mttkrp_ozaki_kernel<false><<<grid, kThreads, kSmemBytes, stream>>>(o.map, mapL, o.rmap, a);
   CALS_CUDA_TRY(cudaGetLastError());
   if (p.S > 1) {
     const long long pairs = p.M * ((cap + 1) / 2);
