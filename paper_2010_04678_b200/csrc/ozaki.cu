@@ -101,10 +101,13 @@ __global__ void oz_slice_rows_kernel(const double* __restrict__ x, long long sm,
 // over all p by every chunk's block (L2-resident, 8 loads per thread).
 __global__ void oz_slice_cols_kernel(const double* __restrict__ lo, long long ld, int Dp, int Kp,
                                      const int* width_ptr, int width, long long cap_pad,
-                                     uint8_t* __restrict__ ls, int* __restrict__ cex) {
+                                     uint8_t* __restrict__ ls, int* __restrict__ cex,
+                                     int* __restrict__ queue) {
   __shared__ double tile[32][33];
   __shared__ double red[8][33];
   __shared__ int ex[32];
+  // the contraction kernel that follows claims its work units from *queue
+  if (blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0) *queue = 0;
   const int W = width_ptr ? *width_ptr : width;
   const int c0 = blockIdx.x * 32, p0 = blockIdx.y * 32;
   if (c0 >= W) return;
@@ -337,12 +340,13 @@ int launch_contraction_ozaki(Tensor& t, const ModePlan& p, int key, const double
   uint8_t* ls = reinterpret_cast<uint8_t*>(oz_ws);
   int* cex = reinterpret_cast<int*>(
       (reinterpret_cast<uintptr_t>(ls + size_t(kSlices) * cap_pad * o.Kp) + 255) & ~uintptr_t(255));
+  int* queue = cex + cap_pad;  // inside the cap_pad * 8 bytes reserved after the slices
   const int sms = sm_count(t.device);
 
   oz_slice_cols_kernel<<<dim3((unsigned)((cap + 31) / 32), (unsigned)(o.Kp / 32)), 256, 0,
                          stream>>>(
       lo, lo_ld, (int)std::min<long long>(lrows, p.Dp), (int)o.Kp, width_ptr, width, cap_pad, ls,
-      cex);
+      cex, queue);
   CALS_CUDA_TRY(cudaGetLastError());
 
   CUtensorMap mapL;
@@ -374,6 +378,7 @@ int launch_contraction_ozaki(Tensor& t, const ModePlan& p, int key, const double
   a.tm_full = mt.tm_full;
   a.rem_rows = mt.rem_rows;
   a.rem_slabs = mt.rem_slabs;
+  a.queue = queue;
 #ifdef CALS_OZ_PROFILE
   // profiling builds: per-CTA cycle counters of the previous launch on stderr
   static unsigned long long* prof = nullptr;

@@ -73,7 +73,11 @@ __device__ __forceinline__ long long prof_clock() { return kProfile ? clock64() 
 // cross-slab FP64 accumulator of the epilogue: [32 rows m][256 epilogue threads]
 constexpr size_t kAccBytes = size_t(32) * 32 * kEpiWarps * 8;
 constexpr size_t kSmemBytes =
-    size_t(STAGES) * kStageBytes + kAccBytes + 1024 /*align*/ + 256 /*barriers*/;
+    size_t(STAGES) * kStageBytes + kAccBytes + 1024 /*align*/ + 512 /*barriers, unit ring*/;
+// work units are handed out at run time (atomic counter, largest units
+// first): the producer warp claims the next unit and passes it to the MMA and
+// epilogue warps through a small ring in shared memory
+constexpr int kUnitRing = 4;
 
 struct Args {
   int M;        // tensor rows of the view (output rows)
@@ -99,6 +103,8 @@ struct Args {
   int tm_full;
   int rem_rows;
   int rem_slabs;
+  // unit counter, zeroed by the Lo slicing kernel before every launch
+  int* queue;
   // CALS_OZ_PROFILE builds only: per-CTA cycle counters (MMA waits, epilogue
   // phases) -- see tools/oz_time.py
   unsigned long long* prof;
@@ -210,6 +216,18 @@ __device__ __forceinline__ void drain_pass(uint64_t* tfull, uint64_t* tempty, ui
   }
 }
 
+// Consumer side of the unit ring (MMA warp, epilogue warps): wait for the
+// producer's claim, read it, release the slot.
+__device__ __forceinline__ int next_unit(uint64_t* ufull, uint64_t* uempty, const int* uring,
+                                         int& uslot, uint32_t& uphase, int lane) {
+  mbar_wait(&ufull[uslot], uphase);
+  const int u = uring[uslot];
+  __syncwarp();
+  if (lane == 0) mbar_arrive(&uempty[uslot]);
+  if (++uslot == kUnitRing) { uslot = 0; uphase ^= 1u; }
+  return u;
+}
+
 // ------------------------------------------------------------- main kernel --
 // kSide: the launch writes the per-slab products (dimension-tree partial);
 // a separate instantiation keeps the side-output code out of the other
@@ -228,7 +246,10 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint64_t* empty = full + STAGES;
   uint64_t* tfull = empty + STAGES;
   uint64_t* tempty = tfull + kTmemBufs;
-  uint32_t* tmem_base_slot = reinterpret_cast<uint32_t*>(tempty + kTmemBufs);
+  uint64_t* ufull = tempty + kTmemBufs;
+  uint64_t* uempty = ufull + kUnitRing;
+  int* uring = reinterpret_cast<int*>(uempty + kUnitRing);
+  uint32_t* tmem_base_slot = reinterpret_cast<uint32_t*>(uring + kUnitRing);
 
   if ((smem_u32(smem) & 1023u) != 0) __trap();
   const int W = args.width_ptr ? *args.width_ptr : args.width;
@@ -247,6 +268,10 @@ __global__ void __launch_bounds__(kThreads, 1)
     for (int b = 0; b < kTmemBufs; ++b) {
       mbar_init(&tfull[b], 1);
       mbar_init(&tempty[b], kEpiWarps);
+    }
+    for (int b = 0; b < kUnitRing; ++b) {
+      mbar_init(&ufull[b], 1);
+      mbar_init(&uempty[b], 1 + kEpiWarps);
     }
     fence_barrier_init();
   }
@@ -271,7 +296,18 @@ __global__ void __launch_bounds__(kThreads, 1)
       tma_prefetch_desc(&tmR);
       const uint32_t rem_tx =
           uint32_t(kLoStageBytes + kSlices * KSTEP * args.rem_rows * args.rem_slabs);
-      for (int u = blockIdx.x; u < units; u += gridDim.x) {
+      int uslot = 0;
+      uint32_t uphase = 0;
+      for (;;) {
+        // claim the next unit (units are numbered largest first: full tiles,
+        // then the one-pass remainder tiles) and publish it to the ring
+        mbar_wait(&uempty[uslot], uphase ^ 1u);
+        int u = atomicAdd(args.queue, 1);
+        if (u >= units) u = -1;
+        uring[uslot] = u;
+        mbar_arrive(&ufull[uslot]);
+        if (++uslot == kUnitRing) { uslot = 0; uphase ^= 1u; }
+        if (u < 0) break;
         const Unit U = unit_decode(u, tn, args);
         const int passes = U.rem ? 1 : U.qe - U.qb;
         for (int i = 0; i < passes; ++i) {
@@ -309,7 +345,11 @@ __global__ void __launch_bounds__(kThreads, 1)
     const uint64_t sdesc = desc_sw32(smem_u32(smem));
     long long w_full = 0, w_tempty = 0;
     const long long t_start = prof_clock();
-    for (int u = blockIdx.x; u < units; u += gridDim.x) {
+    int uslot = 0;
+    uint32_t uphase = 0;
+    for (;;) {
+      const int u = next_unit(ufull, uempty, uring, uslot, uphase, lane);
+      if (u < 0) break;
       const Unit U = unit_decode(u, tn, args);
       const int passes = U.rem ? 1 : U.qe - U.qb;
       for (int i = 0; i < passes; ++i, ++slab) {
@@ -401,7 +441,11 @@ __global__ void __launch_bounds__(kThreads, 1)
     uint32_t slab = 0;
     long long ew_wait = 0, ew_load = 0, ew_final = 0;
     const long long e_start = prof_clock();
-    for (int u = blockIdx.x; u < units; u += gridDim.x) {
+    int uslot = 0;
+    uint32_t uphase = 0;
+    for (;;) {
+      const int u = next_unit(ufull, uempty, uring, uslot, uphase, lane);
+      if (u < 0) break;
       const Unit U = unit_decode(u, tn, args);
       const int c = U.tc * BMC + quad * 32 + lane;
       const bool cval = c < W;
