@@ -765,7 +765,7 @@ static int setup_tree(Engine* e) {
     p.role = kRoleFirstQP;
     p.Dp = t.dims[2];
     p.Dq = t.dims[1];
-    p.S = t.plans[0].S > 1 ? (int)std::min<long long>(p.Dq, t.plans[0].S) : 1;  // CALS_SPLITS
+    p.S = plan_splits(p);
     p.lo_modes = {2};
     p.hi_modes = {1};
   } else {

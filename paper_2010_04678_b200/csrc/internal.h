@@ -68,6 +68,7 @@ int tensor_create(int order, const int64_t* dims, const double* host, const doub
 void tensor_destroy(Tensor* t);
 int tensor_sqnorm(Tensor* t, cudaStream_t stream, double* out);
 ModePlan make_plan(const Tensor& t, int mode);
+int plan_splits(const ModePlan& view);  // shape-only q-split count of a view
 
 // MTTKRP variants ------------------------------------------------------------
 struct VariantInfo {
@@ -110,6 +111,7 @@ int launch_contraction(Tensor& t, const ModePlan& p, int map_key, const double* 
 // Ozaki-sliced INT8 tensor-core contraction (ozaki.cu) ------------------------
 bool ozaki_enabled();                       // CALS_MTTKRP=dmma disables it
 bool ozaki_eligible(const ModePlan& p);
+int ozaki_refine_splits(const ModePlan& p);  // shape-only split count for an INT8 view
 size_t ozaki_ws_bytes(const ModePlan& p, long long cap);  // per-call Lo slices
 double ozaki_tensor_ops(const ModePlan& p, long long width);  // INT8 ops per launch
 // Build (once per tensor and key) the X slices of view `p`; stream-ordered.

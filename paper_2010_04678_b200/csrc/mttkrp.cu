@@ -164,16 +164,23 @@ ModePlan make_plan(const Tensor& t, int mode) {
     for (int i = 0; i < mode; ++i) p.lo_modes.push_back(i);
     for (int i = mode + 1; i < N; ++i) p.hi_modes.push_back(i);
   }
-  // q splits: a function of the shape only (never of the active width) so the
-  // fused result of a column block is bitwise independent of its neighbours.
-  static const int max_splits = [] {
-    const char* env = getenv("CALS_SPLITS");  // tuning knob; still shape-only
-    const int v = env ? atoi(env) : 0;
-    return v > 0 ? v : 32;
-  }();
-  p.S = (int)std::min<long long>(p.Dq, max_splits);
-  if (p.S < 1) p.S = 1;
+  p.S = plan_splits(p);
   return p;
+}
+
+// q splits: a function of the shape only (never of the active width) so the
+// fused result of a column block is bitwise independent of its neighbours.
+// CALS_SPLITS fixes the count (tuning knob; still shape-only); otherwise 32,
+// refined for INT8 views whose leftover rows pack better with another count.
+int plan_splits(const ModePlan& view) {
+  static const int env_splits = [] {
+    const char* env = getenv("CALS_SPLITS");
+    return env ? atoi(env) : 0;
+  }();
+  ModePlan p = view;
+  p.S = (int)std::max<long long>(1, std::min<long long>(p.Dq, env_splits > 0 ? env_splits : 32));
+  if (env_splits <= 0 && ozaki_eligible(p)) p.S = ozaki_refine_splits(p);
+  return p.S;
 }
 
 __global__ void pad_copy_kernel(const double* __restrict__ src, long long i0, long long i0p,

@@ -199,6 +199,37 @@ static MTiling m_tiling(const ModePlan& p) {
   return {int((p.M + BNM - 1) / BNM), 0, 0};
 }
 
+// Split count for an INT8 view (shape only): among 24..48 splits, the one
+// minimising the 64-row tile passes (the packed remainder tile is one pass per
+// split, and only packs when M % 64 rows x slabs per split fit 64 columns)
+// plus the split reduction's traffic (S partial blocks, ~49 / (Dq Kp) of the
+// contraction time each, measured at c2).  c2 (200^3): 25 splits, 8 slabs
+// each, the 8 leftover rows of a split fill a whole remainder tile (625 instead
+// of 632 passes per column tile, 25 instead of 32 partials).  Views where no
+// count packs better keep the default.
+int ozaki_refine_splits(const ModePlan& base) {
+  auto passes = [&](int S) {
+    ModePlan q = base;
+    q.S = S;
+    const MTiling mt = m_tiling(q);
+    return double(mt.tm_full) * double(q.Dq) + (mt.rem_rows ? double(S) : 0.0);
+  };
+  const double kp = double(kp_of(base.Dp));
+  auto cost = [&](int S) { return passes(S) * (1.0 + 49.0 * S / (double(base.Dq) * kp)); };
+  const double p0 = passes(base.S);
+  int best = base.S;
+  double best_cost = cost(base.S);
+  for (int S = 24; S <= 48 && 3LL * S <= base.Dq; ++S) {
+    if (passes(S) > 0.995 * p0) continue;  // only a real packing gain moves it
+    const double c = cost(S);
+    if (c < best_cost) {
+      best_cost = c;
+      best = S;
+    }
+  }
+  return best;
+}
+
 // 28 slice products x 2 ops per MAC over the padded tiles the kernel runs
 double ozaki_tensor_ops(const ModePlan& p, long long width) {
   const MTiling mt = m_tiling(p);
