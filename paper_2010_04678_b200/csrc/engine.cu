@@ -13,6 +13,7 @@
 // replays the graph and polls a mapped "done" flag; no per-iteration host
 // round trip.
 #include <algorithm>
+#include <climits>
 #include <chrono>
 #include <cstring>
 #include <numeric>
@@ -129,6 +130,13 @@ __device__ inline void decide_model(EngState* st, int k, double e) {
 // ------------------------------------------------------------------ update --
 // RB > 0: fast path (every rank <= RB, rows in registers, chunked Gram);
 // RB == 0: generic path for ranks up to 128.  Same reference semantics.
+#ifdef CALS_UPD_PROFILE
+__device__ long long g_upd_prof[3][4096][13];
+#define UPD_STAMP(i) \
+  if (threadIdx.x == 32) ustamp[i] = clock64();
+#else
+#define UPD_STAMP(i)
+#endif
 template <int RB>
 __global__ void __launch_bounds__(kUpdThreads, 2) engine_update_kernel(EngState* st_g, int n,
                                                                      int nthr) {
@@ -140,9 +148,15 @@ __global__ void __launch_bounds__(kUpdThreads, 2) engine_update_kernel(EngState*
   // is then one smem load instead of a dependent global round trip.  Writes
   // go through the copied pointers into the global arrays.
   __shared__ __align__(16) EngState sst;
+#ifdef CALS_UPD_PROFILE
+  __shared__ long long ustamp[10];
+  const long long t_entry = (long long)globaltimer_ns();
+  const long long c_entry = clock64();
+#endif
   for (int i = threadIdx.x; i < int(sizeof(EngState) / 4); i += blockDim.x)
     reinterpret_cast<int*>(&sst)[i] = reinterpret_cast<const int*>(st_g)[i];
   __syncthreads();
+  UPD_STAMP(0)
   EngState* const st = &sst;
   const int N = st->order;
   const int Rmax = st->max_rank;
@@ -161,12 +175,13 @@ __global__ void __launch_bounds__(kUpdThreads, 2) engine_update_kernel(EngState*
     const int off = st->slot_off[slot];
     const long long go = st->gram_off[k];
     auto gram = [&](int i) { return st->grams + i * st->gram_stride + go; };
+    UPD_STAMP(1)
 
     if (n == 0 && st->fresh[k]) {
       // Gramians of the admitted starting point (driver.py:203-205)
       for (int i = 1; i < N; ++i) {
         if constexpr (RB > 0)
-          block_gram_fast(st->F[i] + off, ld, (int)st->dims[i], R, X, gram(i));
+          block_gram_fast<RB>(st->F[i] + off, ld, (int)st->dims[i], R, X, gram(i));
         else
           block_gram(st->F[i], ld, off, (int)st->dims[i], R, gram(i));
       }
@@ -206,8 +221,9 @@ __global__ void __launch_bounds__(kUpdThreads, 2) engine_update_kernel(EngState*
         // stage its first chunk of rows into X (the reference checks before
         // touching anything, als.py:84-85; a NaN pivot is caught below too)
         __syncthreads();
+        UPD_STAMP(2)
         if (threadIdx.x < 32) {
-          warp_cholesky_fast_nosync(H, R, inv_diag, &flag);
+          warp_cholesky_fast_nosync<RB>(H, R, inv_diag, &flag);
         } else {
           const int P = fast_pitch(R);
           const int nt = blockDim.x - 32;
@@ -223,7 +239,9 @@ __global__ void __launch_bounds__(kUpdThreads, 2) engine_update_kernel(EngState*
           for (int a = 0; a < R; ++a) bad |= !isfinite(mrow[a]);
         }
       }
-      if (__syncthreads_or(bad)) {
+      const int any_bad = __syncthreads_or(bad);
+      UPD_STAMP(3)
+      if (any_bad) {
         // non-finite input: the reference raises ValueError -> FAILED (als.py:84-85)
         if (threadIdx.x == 0) st->failed[k] = 1;
         __syncthreads();
@@ -249,16 +267,21 @@ __global__ void __launch_bounds__(kUpdThreads, 2) engine_update_kernel(EngState*
             }
           }
           __syncthreads();
-          block_gram_fast(st->F[n] + off, ld, rows, R, X, gram(n));
+          block_gram_fast<(RB > 0 ? RB : kFastR)>(st->F[n] + off, ld, rows, R, X, gram(n));
           done = true;
         }
         if constexpr (RB > 0) {
           chol_ok = !done && flag != 0;
           if (chol_ok) {
-            done = block_solve_gram_fast(H, inv_diag, R, Mb, ld, rows, st->F[n] + off, ld, X,
-                                         gram(n), n == N - 1, &inner, red, true);
+            done = block_solve_gram_fast<RB>(H, inv_diag, R, Mb, ld, rows, st->F[n] + off, ld, X,
+                                         gram(n), n == N - 1, &inner, red, true
+#ifdef CALS_UPD_PROFILE
+                                         , ustamp + 6
+#endif
+            );
             have_inner = done && n == N - 1;
           }
+          UPD_STAMP(4)
         }
         if (!done) {
           for (int idx = threadIdx.x; idx < R * R; idx += blockDim.x) H[idx] = Hsave[idx];
@@ -270,6 +293,7 @@ __global__ void __launch_bounds__(kUpdThreads, 2) engine_update_kernel(EngState*
       }
       __syncthreads();
     }
+    UPD_STAMP(5)
     if (n == N - 1) {
       // fast error / fit / stopping rule (driver.py:241-273, als.py:99-124)
       double msq = 0.0;
@@ -302,6 +326,15 @@ __global__ void __launch_bounds__(kUpdThreads, 2) engine_update_kernel(EngState*
       }
       __syncthreads();
     }
+#ifdef CALS_UPD_PROFILE
+    if (threadIdx.x == 0 && slot < 4096 && n < 3) {
+      g_upd_prof[n][slot][0] = t_entry;
+      g_upd_prof[n][slot][1] = (long long)globaltimer_ns();
+      g_upd_prof[n][slot][2] = clock64() - c_entry;
+      g_upd_prof[n][slot][3] = R;
+      for (int i = 0; i < 9; ++i) g_upd_prof[n][slot][4 + i] = ustamp[i] - c_entry;
+    }
+#endif
   }
 }
 
@@ -414,6 +447,11 @@ __global__ void __launch_bounds__(kUpdThreads) ls_finish_kernel(EngState* st) {
 
 using UpdateKernel = void (*)(EngState*, int, int);
 static UpdateKernel update_kernel_for(int max_rank, int* rb) {
+  // rank buckets: the per-thread register arrays (Cholesky column, solved
+  // row, Gram pairs) are sized to the largest rank of the batch
+  if (max_rank <= 8) { *rb = 8; return engine_update_kernel<8>; }
+  if (max_rank <= 16) { *rb = 16; return engine_update_kernel<16>; }
+  if (max_rank <= 24) { *rb = 24; return engine_update_kernel<24>; }
   if (max_rank <= kFastR) { *rb = kFastR; return engine_update_kernel<kFastR>; }
   *rb = 0;
   return engine_update_kernel<0>;
@@ -1396,8 +1434,39 @@ int cals_engine_load_pool(cals_engine* e, const double* src, int src_is_device, 
 int cals_engine_run(cals_engine* e, double tol, int max_iterations, double sqnorm, int use_graph,
                     void* stream, int* iterations) {
   CALS_CHECK(e, kErrInvalid, "null engine");
-  return engine_run(e->e, tol, max_iterations, sqnorm, use_graph, (cudaStream_t)stream,
-                    iterations);
+  const int rc = engine_run(e->e, tol, max_iterations, sqnorm, use_graph, (cudaStream_t)stream,
+                            iterations);
+#ifdef CALS_UPD_PROFILE
+  {
+    static long long h[3][4096][13];
+    cudaDeviceSynchronize();
+    cudaMemcpyFromSymbol(h, g_upd_prof, sizeof(h));
+    const int ns = std::min(e->e->n_models, 4096);
+    for (int n = 0; n < 3; ++n) {
+      long long t0 = LLONG_MAX, t0max = 0, t1 = 0, cmax = 0, csum = 0;
+      int cnt = 0;
+      for (int sl = 0; sl < ns; ++sl) {
+        const long long* p = h[n][sl];
+        if (p[1] <= p[0]) continue;
+        t0 = std::min(t0, p[0]); t0max = std::max(t0max, p[0]); t1 = std::max(t1, p[1]);
+        cmax = std::max(cmax, p[2]); csum += p[2]; ++cnt;
+      }
+      fprintf(stderr, "[updprof] mode %d: span %lld ns, last block entry +%lld ns, block clk max %lld mean %lld\n",
+              n, t1 - t0, t0max - t0, cmax, cnt ? csum / cnt : 0);
+      // mean stamps (clk since entry): state copy, slot loads, H, chol+stage, solve+gram, pre-error
+      long long ms[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
+      for (int sl = 0; sl < ns; ++sl)
+        for (int i = 0; i < 9; ++i) ms[i] += h[n][sl][4 + i];
+      if (cnt)
+        fprintf(stderr, "[updprof]   mean stamps: sst %lld, slot %lld, H %lld, chol+stage %lld, solve+gram %lld, pre-err %lld, end %lld\n",
+                ms[0] / cnt, ms[1] / cnt, ms[2] / cnt, ms[3] / cnt, ms[4] / cnt, ms[5] / cnt, csum / cnt);
+      if (cnt)
+        fprintf(stderr, "[updprof]   inside solve+gram: solved %lld, written %lld, gram %lld\n",
+                ms[6] / cnt, ms[7] / cnt, ms[8] / cnt);
+    }
+  }
+#endif
+  return rc;
 }
 
 int cals_engine_results(cals_engine* e, double* pool, int32_t* status, int32_t* iterations,

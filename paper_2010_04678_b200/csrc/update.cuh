@@ -243,12 +243,16 @@ constexpr int kFastNP = (kFastR * (kFastR + 1) / 2 + kUpdThreads - 1) / kUpdThre
 
 __device__ __forceinline__ int fast_pitch(int R) { return (R & 1) ? R : R + 1; }
 
-struct FastPairs {
-  int a[kFastNP], b[kFastNP];
-  double acc[kFastNP];
+// pairs per thread for rank bucket RB
+__host__ __device__ constexpr int fast_np(int RB) { return (RB * (RB + 1) / 2 + kUpdThreads - 1) / kUpdThreads; }
+template <int NP>
+struct FastPairsT {
+  int a[NP], b[NP];
+  double acc[NP];
   __device__ void init(int R) {
     const int npairs = R * (R + 1) / 2;
-    for (int j = 0; j < kFastNP; ++j) {
+#pragma unroll
+    for (int j = 0; j < NP; ++j) {
       const int p = threadIdx.x + j * kUpdThreads;
       acc[j] = 0.0;
       a[j] = -1;
@@ -265,7 +269,8 @@ struct FastPairs {
     }
   }
   __device__ void accumulate(const double* Xs, int P, int cnt) {
-    for (int j = 0; j < kFastNP; ++j) {
+#pragma unroll
+    for (int j = 0; j < NP; ++j) {
       if (a[j] < 0) continue;
       const double* pa = Xs + a[j];
       const double* pb = Xs + b[j];
@@ -285,7 +290,8 @@ struct FastPairs {
     }
   }
   __device__ void store(double* G, int R) const {
-    for (int j = 0; j < kFastNP; ++j) {
+#pragma unroll
+    for (int j = 0; j < NP; ++j) {
       if (a[j] < 0) continue;
       G[a[j] * R + b[j]] = acc[j];
       G[b[j] * R + a[j]] = acc[j];
@@ -301,13 +307,18 @@ struct FastPairs {
 // H[a][b] -= U[k][a] U[k][b] with U[k][a] broadcast by shuffles.  U is
 // written back over the upper triangle; inv_diag[k] = 1/U[k][k].  Fails like
 // dpotrf (pivot <= 0 or NaN).
-__device__ inline void warp_cholesky_fast_nosync(double* __restrict__ H, int R,
+template <int RB>
+__device__ __forceinline__ void warp_cholesky_rb(double* __restrict__ H, int R,
                                                  double* __restrict__ inv_diag, int* flag) {
   const int lane = threadIdx.x;
-  double col[32];
+  double col[RB];  // lane b: column b, rows k.. (rotated: col[0] is the pivot row)
 #pragma unroll
-  for (int a = 0; a < 32; ++a) col[a] = (a < R && lane < R && a <= lane) ? H[a * R + lane] : 0.0;
+  for (int a = 0; a < RB; ++a) col[a] = (a < R && lane < R && a <= lane) ? H[a * R + lane] : 0.0;
   bool ok = true;
+  // The k loop stays rolled: one compact body (RB - 1 shuffles and FMAs, a
+  // register rotation) executed R times.  A fully unrolled triangle is
+  // ~3x slower here -- a single warp streaming tens of KB of straight-line
+  // code misses the instruction cache on every line.
   for (int k = 0; k < R; ++k) {
     const double piv = __shfl_sync(0xffffffffu, col[0], k);
     if (!(piv > 0.0)) {
@@ -320,18 +331,34 @@ __device__ inline void warp_cholesky_fast_nosync(double* __restrict__ H, int R,
     if (lane >= k && lane < R) H[k * R + lane] = ukb;
     if (lane == 0) inv_diag[k] = inv;
 #pragma unroll
-    for (int a = 1; a < 32; ++a) {
+    for (int a = 1; a < RB; ++a) {
       // U[k][k + a] from lane k + a (0 past the matrix)
       const int src = k + a;
       const double uka = __shfl_sync(0xffffffffu, ukb, src < 32 ? src : 31);
       if (src <= lane && src < R) col[a] = fma(-uka, ukb, col[a]);
     }
 #pragma unroll
-    for (int a = 0; a < 31; ++a) col[a] = col[a + 1];
-    col[31] = 0.0;
+    for (int a = 0; a < RB - 1; ++a) col[a] = col[a + 1];
+    col[RB - 1] = 0.0;
   }
   __syncwarp();
   if (lane == 0) *flag = ok ? 1 : 0;
+}
+
+// rank buckets up to RB (a kernel built for bucket RB only holds RB-sized
+// register arrays)
+template <int RB = kFastR>
+__device__ __forceinline__ void warp_cholesky_fast_nosync(double* __restrict__ H, int R,
+                                                          double* __restrict__ inv_diag,
+                                                          int* flag) {
+  if (RB <= 8 || R <= 8)
+    warp_cholesky_rb<8>(H, R, inv_diag, flag);
+  else if (RB <= 16 || R <= 16)
+    warp_cholesky_rb<16>(H, R, inv_diag, flag);
+  else if (RB <= 24 || R <= 24)
+    warp_cholesky_rb<24>(H, R, inv_diag, flag);
+  else
+    warp_cholesky_rb<32>(H, R, inv_diag, flag);
 }
 
 __device__ inline bool warp_cholesky_fast(double* H, int R, double* inv_diag, int* flag) {
@@ -369,10 +396,11 @@ __device__ __forceinline__ int stage_block(const double* __restrict__ Mb, long l
 }
 
 // Gram of an existing column block (rows x R at F + off), chunked through Xs.
+template <int RB = kFastR>
 __device__ inline void block_gram_fast(const double* F, long long ld, int rows, int R, double* Xs,
                                        double* G) {
   const int P = fast_pitch(R);
-  FastPairs pr;
+  FastPairsT<fast_np(RB)> pr;
   pr.init(R);
   for (int base = 0; base < rows; base += kUpdThreads) {
     const int cnt = min(kUpdThreads, rows - base);
@@ -385,11 +413,10 @@ __device__ inline void block_gram_fast(const double* F, long long ld, int rows, 
 }
 
 // One row's two triangular solves (U^T y = m, then U x = y; dpotrs order,
-// reciprocal diagonal) with the row in registers: the loops are unrolled to
-// the rank bucket RB (static register indices; steps beyond R are skipped by
-// a block-uniform branch), so each step is a chain of one multiply and the
-// independent FMAs of the remaining entries instead of shared-memory
-// read-modify-writes.  Same operation order as the shared-memory version.
+// reciprocal diagonal) with the row in registers (rank bucket RB), so each
+// step is a chain of one multiply and the independent FMAs of the remaining
+// entries instead of shared-memory read-modify-writes.  Same operation order
+// per entry as the shared-memory version (bitwise identical).
 template <int RB>
 __device__ __forceinline__ void solve_row_reg(double* __restrict__ xs,
                                               const double* __restrict__ U,
@@ -422,39 +449,17 @@ __device__ __forceinline__ void solve_row_reg(double* __restrict__ xs,
     if (a < R) xs[a] = x[a];
 }
 
-__device__ __forceinline__ void solve_row_smem(double* __restrict__ x,
-                                               const double* __restrict__ U,
-                                               const double* __restrict__ inv_diag, int R) {
-  for (int k = 0; k < R; ++k) {  // U^T y = m
-    const double xk = x[k] * inv_diag[k];
-    x[k] = xk;
-    const double* urow = U + k * R;
-#pragma unroll 4
-    for (int a = k + 1; a < R; ++a) x[a] = fma(-urow[a], xk, x[a]);
-  }
-  for (int k = R - 1; k >= 0; --k) {  // U x = y
-    const double xk = x[k] * inv_diag[k];
-    x[k] = xk;
-#pragma unroll 4
-    for (int a = 0; a < k; ++a) x[a] = fma(-U[a * R + k], xk, x[a]);
-  }
-}
-
-// Solve every row of the block against U (smem) / inv_diag, write A,
-// refresh G = A^T A and (want_inner) return sum(A o M).  Returns false when
-// a solution entry is non-finite (caller -> pinv path).  Rows go through Xs
-// in chunks of kUpdThreads: coalesced stage -> one thread per row solves in
-// place -> coalesced write-back (+ inner product against M) -> Gram pairs.
+template <int RB = kFastR>
 __device__ __forceinline__ bool block_solve_gram_fast(const double* __restrict__ U,
                                              const double* __restrict__ inv_diag, int R,
                                              const double* __restrict__ Mb, long long ldm,
                                              int rows, double* __restrict__ A, long long lda,
                                              double* __restrict__ Xs, double* __restrict__ G,
                                              bool want_inner, double* inner, double* red,
-                                             bool first_chunk_staged = false) {
+                                             bool first_chunk_staged = false,
+                                             long long* stamps = nullptr) {
   const int P = fast_pitch(R);
-  FastPairs pr;
-  pr.init(R);
+  FastPairsT<fast_np(RB)> pr;
   double dot = 0.0;
   int bad = 0;
   for (int base = 0; base < rows; base += kUpdThreads) {
@@ -466,16 +471,17 @@ __device__ __forceinline__ bool block_solve_gram_fast(const double* __restrict__
     }
     if (threadIdx.x < cnt) {
       double* x = Xs + threadIdx.x * P;
-      if (R <= 8)
+      if (RB <= 8 || R <= 8)
         solve_row_reg<8>(x, U, inv_diag, R);
-      else if (R <= 16)
+      else if (RB <= 16 || R <= 16)
         solve_row_reg<16>(x, U, inv_diag, R);
-      else if (R <= 24)
+      else if (RB <= 24 || R <= 24)
         solve_row_reg<24>(x, U, inv_diag, R);
-      else  // 25..32: shared-memory rows (a 32-entry register row spills)
-        solve_row_smem(x, U, inv_diag, R);
+      else
+        solve_row_reg<32>(x, U, inv_diag, R);
     }
     __syncthreads();
+    if (stamps && threadIdx.x == 32) stamps[0] = clock64();
     double* Ac = A + (long long)base * lda;
     const int total = cnt * R;
     for (int e = threadIdx.x; e < total; e += kUpdThreads) {
@@ -485,8 +491,11 @@ __device__ __forceinline__ bool block_solve_gram_fast(const double* __restrict__
       Ac[(long long)i * lda + a] = v;
       if (want_inner) dot = fma(v, Mc[(long long)i * ldm + a], dot);
     }
+    if (stamps && threadIdx.x == 32) stamps[1] = clock64();
+    if (base == 0) pr.init(R);  // not live across the first chunk's solve
     pr.accumulate(Xs, P, cnt);
     __syncthreads();
+    if (stamps && threadIdx.x == 32) stamps[2] = clock64();
   }
   if (__syncthreads_or(bad)) return false;
   pr.store(G, R);
