@@ -698,11 +698,99 @@ __global__ void partial_ttv_kernel(const double* __restrict__ P, long long ld, l
   }
 }
 
+// The same contraction (out[b] = sum_a P[a + Da b] F[a], 4 output rows per
+// thread) for partials with few output rows and a long a-range (c3's Z tree:
+// 21 rows, a over 251): the a-range is cut into G chunks (threadIdx.y), each
+// summed in ascending order, and the chunk sums are added in chunk order
+// through shared memory -- deterministic and per column, so position
+// independent.  Without the split only rows/4 x W threads exist (1800 at c3).
+__global__ void __launch_bounds__(512) partial_ttv_split_kernel(const double* __restrict__ P, long long ld, long long Da,
+                                         long long La, const double* __restrict__ F,
+                                         long long ldf, const int* width_ptr, int width,
+                                         long long rows_out, double* __restrict__ out,
+                                         long long ldo) {
+  extern __shared__ double red[];  // [G][4][32]
+  const int W = width_ptr ? *width_ptr : width;
+  if ((int)blockIdx.x * 32 >= W) return;  // block-uniform
+  const int G = blockDim.y, tx = threadIdx.x, ty = threadIdx.y;
+  const int c = blockIdx.x * 32 + tx;
+  const long long r4 = (long long)blockIdx.y * 4;
+  const int nr = (int)min(4LL, rows_out - r4);
+  double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+  if (c < W) {
+    const double* p4 = P + r4 * Da * ld + c;
+    const double* f = F + c;
+    const long long rs1 = (nr > 1 ? 1 : 0) * Da * ld, rs2 = (nr > 2 ? 2 : nr - 1) * Da * ld,
+                    rs3 = (nr > 3 ? 3 : nr - 1) * Da * ld;
+    const long long a_lo = La * ty / G, a_hi = La * (ty + 1) / G;
+    long long a = a_lo;
+    for (; a + 4 <= a_hi; a += 4) {
+      double fv[4], pv[4][4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        fv[u] = __ldg(f + (a + u) * ldf);
+        const double* pa = p4 + (a + u) * ld;
+        pv[u][0] = __ldg(pa);
+        pv[u][1] = __ldg(pa + rs1);
+        pv[u][2] = __ldg(pa + rs2);
+        pv[u][3] = __ldg(pa + rs3);
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        a0 = fma(pv[u][0], fv[u], a0);
+        a1 = fma(pv[u][1], fv[u], a1);
+        a2 = fma(pv[u][2], fv[u], a2);
+        a3 = fma(pv[u][3], fv[u], a3);
+      }
+    }
+    for (; a < a_hi; ++a) {
+      const double fa = __ldg(f + a * ldf);
+      const double* pa = p4 + a * ld;
+      a0 = fma(__ldg(pa), fa, a0);
+      a1 = fma(__ldg(pa + rs1), fa, a1);
+      a2 = fma(__ldg(pa + rs2), fa, a2);
+      a3 = fma(__ldg(pa + rs3), fa, a3);
+    }
+  }
+  double* rd = red + (size_t)ty * 128 + tx;
+  rd[0] = a0;
+  rd[32] = a1;
+  rd[64] = a2;
+  rd[96] = a3;
+  __syncthreads();
+  if (ty == 0 && c < W) {
+    double s0 = a0, s1 = a1, s2 = a2, s3 = a3;
+    for (int g = 1; g < G; ++g) {
+      const double* q = red + (size_t)g * 128 + tx;
+      s0 += q[0];
+      s1 += q[32];
+      s2 += q[64];
+      s3 += q[96];
+    }
+    double* o = out + r4 * ldo + c;
+    o[0] = s0;
+    if (nr > 1) o[ldo] = s1;
+    if (nr > 2) o[2 * ldo] = s2;
+    if (nr > 3) o[3 * ldo] = s3;
+  }
+}
+
 int launch_partial_ttv(const double* P, long long ld, long long Da, long long Db, int reduce_b,
                        long long La, const double* F, long long ldf, int width,
                        const int* width_ptr, long long cap, long long rows_out, double* out,
                        long long ldo, int sms, cudaStream_t stream) {
   const long long n = rows_out * cap;
+  if (!reduce_b) {
+    const long long threads = (rows_out + 3) / 4 * cap;
+    const long long G = std::min<long long>({16, 65536 / std::max<long long>(1, threads), La / 8});
+    if (G >= 2) {
+      const dim3 grid((unsigned)((cap + 31) / 32), (unsigned)((rows_out + 3) / 4));
+      partial_ttv_split_kernel<<<grid, dim3(32, (unsigned)G), size_t(G) * 128 * 8, stream>>>(
+          P, ld, Da, La, F, ldf, width_ptr, width, rows_out, out, ldo);
+      CALS_CUDA_TRY(cudaGetLastError());
+      return kOk;
+    }
+  }
   const int blocks = (int)std::max<long long>(1, std::min<long long>(sms * 16, (n + 255) / 256));
   partial_ttv_kernel<<<blocks, 256, 0, stream>>>(P, ld, Da, Db, reduce_b, La, F, ldf, width_ptr,
                                                  width, rows_out, out, ldo);
