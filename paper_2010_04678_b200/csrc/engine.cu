@@ -48,6 +48,10 @@ struct EngState {
   // slots
   int* slot_model;
   int* slot_off;
+  // per slot {model, rank, column offset, Gramian offset}: written by the plan
+  // kernel next to slot_model / slot_off, read by the update kernel in one
+  // load (no slot -> model -> rank / offset dependent round trips)
+  int4* slot_info;
   // move plan
   int* mv_kind;
   int* mv_model;
@@ -138,8 +142,8 @@ __device__ long long g_upd_prof[3][4096][13];
 #define UPD_STAMP(i)
 #endif
 template <int RB>
-__global__ void __launch_bounds__(kUpdThreads, 2) engine_update_kernel(EngState* st_g, int n,
-                                                                     int nthr) {
+__global__ void __launch_bounds__(kUpdThreads, 2) engine_update_kernel(
+    EngState* st_g, const int4* __restrict__ slot_info, int n, int nthr) {
   extern __shared__ __align__(16) double dsm[];
   __shared__ int flag;
   __shared__ double red[kUpdThreads];
@@ -153,6 +157,9 @@ __global__ void __launch_bounds__(kUpdThreads, 2) engine_update_kernel(EngState*
   const long long t_entry = (long long)globaltimer_ns();
   const long long c_entry = clock64();
 #endif
+  // this block's first slot record is loaded alongside the state copy
+  // (blockIdx.x < max_slots: always in bounds; used only if the slot is active)
+  const int4 si_first = slot_info[blockIdx.x];
   for (int i = threadIdx.x; i < int(sizeof(EngState) / 4); i += blockDim.x)
     reinterpret_cast<int*>(&sst)[i] = reinterpret_cast<const int*>(st_g)[i];
   __syncthreads();
@@ -170,10 +177,11 @@ __global__ void __launch_bounds__(kUpdThreads, 2) engine_update_kernel(EngState*
   const int n_active = st->n_active;
 
   for (int slot = blockIdx.x; slot < n_active; slot += gridDim.x) {
-    const int k = st->slot_model[slot];
-    const int R = st->rank[k];
-    const int off = st->slot_off[slot];
-    const long long go = st->gram_off[k];
+    const int4 si = slot == (int)blockIdx.x ? si_first : slot_info[slot];
+    const int k = si.x;
+    const int R = si.y;
+    const int off = si.z;
+    const long long go = si.w;
     auto gram = [&](int i) { return st->grams + i * st->gram_stride + go; };
     UPD_STAMP(1)
 
@@ -445,7 +453,7 @@ __global__ void __launch_bounds__(kUpdThreads) ls_finish_kernel(EngState* st) {
   }
 }
 
-using UpdateKernel = void (*)(EngState*, int, int);
+using UpdateKernel = void (*)(EngState*, const int4*, int, int);
 static UpdateKernel update_kernel_for(int max_rank, int* rb) {
   // rank buckets: the per-thread register arrays (Cholesky column, solved
   // row, Gram pairs) are sized to the largest rank of the batch
@@ -513,6 +521,7 @@ __global__ void __launch_bounds__(kPlanThreads, 1) engine_plan_kernel(EngState* 
     const int k = valid ? st->slot_model[s] : 0;
     const int src = valid ? st->slot_off[s] : 0;
     const int rank_k = valid ? st->rank[k] : 0;
+    const int gram_k = valid ? (int)st->gram_off[k] : 0;
     const bool retiring = valid && st->status[k] != kActive;
     const bool keep = valid && !retiring;
     const int new_w = s_new_w, new_n = s_new_n, retired = s_retired, moves = s_moves,
@@ -545,6 +554,7 @@ __global__ void __launch_bounds__(kPlanThreads, 1) engine_plan_kernel(EngState* 
         // of this chunk was read before the barrier above
         st->slot_model[new_n + kidx] = k;
         st->slot_off[new_n + kidx] = dst_keep;
+        st->slot_info[new_n + kidx] = make_int4(k, rank_k, dst_keep, gram_k);
       }
     }
     if (threadIdx.x == 0) {
@@ -567,6 +577,7 @@ __global__ void __launch_bounds__(kPlanThreads, 1) engine_plan_kernel(EngState* 
       st->t_admit[k] = now;
       st->slot_model[new_n] = k;
       st->slot_off[new_n] = new_w;
+      st->slot_info[new_n] = make_int4(k, st->rank[k], new_w, (int)st->gram_off[k]);
       st->mv_kind[moves] = kMoveAdmit;
       st->mv_model[moves] = k;
       st->mv_src[moves] = 0;
@@ -877,6 +888,7 @@ static int engine_create(Tensor* t, int capacity, int n_models, const int* ranks
   }
   e->pool_elems = po;
   e->gram_stride = std::max<long long>(go, 1);
+  CALS_CHECK(e->gram_stride < (1LL << 31), kErrUnsupported, "Gramian arena beyond 2^31 entries");
   e->lam_elems = std::max<long long>(lo, 1);
   e->trace_cap = std::max(trace_cap, 1);
 
@@ -907,6 +919,7 @@ static int engine_create(Tensor* t, int capacity, int n_models, const int* ranks
   const int mv = 2 * ms + 2;
   items.push_back({(void**)&h.slot_model, size_t(ms) * 4});
   items.push_back({(void**)&h.slot_off, size_t(ms) * 4});
+  items.push_back({(void**)&h.slot_info, size_t(ms) * 16});
   items.push_back({(void**)&h.mv_kind, size_t(mv) * 4});
   items.push_back({(void**)&h.mv_model, size_t(mv) * 4});
   items.push_back({(void**)&h.mv_src, size_t(mv) * 4});
@@ -1064,7 +1077,8 @@ static int enqueue_mode_mttkrp(Engine* e, int n, cudaStream_t stream) {
 }
 
 static int enqueue_mode_update(Engine* e, int n, cudaStream_t stream) {
-  e->upd_kernel<<<e->upd_grid, kUpdThreads, e->upd_smem, stream>>>(e->d_st, n, e->upd_nthr);
+  e->upd_kernel<<<e->upd_grid, kUpdThreads, e->upd_smem, stream>>>(e->d_st, e->h_st.slot_info,
+                                                                   n, e->upd_nthr);
   CALS_CUDA_TRY(cudaGetLastError());
   return kOk;
 }

@@ -20,16 +20,19 @@ namespace cals {
 
 constexpr int kUpdThreads = 256;
 
-// deterministic block sum (fixed tree); `red` has >= blockDim.x doubles
+// Deterministic block sum (blockDim.x a multiple of 32; `red` has >= 32
+// doubles): an xor butterfly inside each warp (partners add the same two
+// values, so every lane holds the same bits), then the warp sums in warp
+// order.  Two barriers instead of a log2(blockDim) smem tree.
 __device__ __forceinline__ double block_sum(double v, double* red) {
-  red[threadIdx.x] = v;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  const int nw = blockDim.x >> 5;
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v;
   __syncthreads();
-  for (int w = blockDim.x / 2; w > 0; w >>= 1) {
-    if (threadIdx.x < w) red[threadIdx.x] += red[threadIdx.x + w];
-    __syncthreads();
-  }
-  const double s = red[0];
-  __syncthreads();
+  double s = red[0];
+  for (int i = 1; i < nw; ++i) s += red[i];
+  __syncthreads();  // red reusable
   return s;
 }
 
