@@ -48,6 +48,13 @@ def test_generic_update_path_ranks_above_32(cals):
     _vs_oracle(cals, (40, 36, 34), [33, 40], 1, 0.0, 4, 80, fac_tol=1e-8)
 
 
+@pytest.mark.parametrize("ranks", [[1, 8], [9, 16], [17, 24], [25, 32]])
+def test_update_rank_buckets(cals, ranks):
+    """The update kernel is instantiated per rank bucket (largest rank of the
+    batch: <= 8 / 16 / 24 / 32); each bucket at both of its ends."""
+    _vs_oracle(cals, (34, 33, 35), ranks, 1, 0.0, 4, sum(ranks), fac_tol=1e-8)
+
+
 def test_refill_churn(cals):
     _vs_oracle(cals, (10, 9, 8), [1, 2, 3], 12, 1e-5, 60, 5, fac_tol=1e-6, seed=7)
 
