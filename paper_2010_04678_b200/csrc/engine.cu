@@ -605,7 +605,9 @@ __global__ void __launch_bounds__(kPlanThreads, 1) engine_plan_kernel(EngState* 
     st->plans_done = rec + 1;
     if (new_n == 0 && head >= st->n_models) {
       st->done = 1;
-      *st->host_done = 1;
+      st->host_done[1] = rec + 1;  // plan count, read by the host without a copy
+      __threadfence_system();
+      st->host_done[0] = 1;
       __threadfence_system();
     }
   }
@@ -719,7 +721,9 @@ struct Engine {
   long long* d_lam_off = nullptr;
   size_t ws_bytes = 0;
   double* d_ws = nullptr;
-  int* h_done = nullptr;  // mapped pinned
+  int* h_done = nullptr;  // mapped pinned: [0] done flag, [1] plans at completion
+  EngState* h_st_pinned = nullptr;  // page-locked staging of the state upload
+  cudaEvent_t st_upload_ev = nullptr;
   char* h_results = nullptr;  // pinned staging of the per-model results
   size_t h_results_bytes = 0;
   int* d_done_alias = nullptr;
@@ -839,6 +843,8 @@ static int engine_free(Engine* e) {
   if (e->d_nnls) cudaFree(e->d_nnls);
   if (e->d_st) cudaFree(e->d_st);
   if (e->h_done) cudaFreeHost(e->h_done);
+  if (e->h_st_pinned) cudaFreeHost(e->h_st_pinned);
+  if (e->st_upload_ev) cudaEventDestroy(e->st_upload_ev);
   if (e->h_results) cudaFreeHost(e->h_results);
   delete e;
   return kOk;
@@ -966,6 +972,8 @@ static int engine_create(Tensor* t, int capacity, int n_models, const int* ranks
   }
   CALS_CUDA_TRY(cudaMalloc(&e->d_st, sizeof(EngState)));
   CALS_CUDA_TRY(cudaHostAlloc(&e->h_done, 64, cudaHostAllocMapped));
+  CALS_CUDA_TRY(cudaHostAlloc(&e->h_st_pinned, sizeof(EngState), cudaHostAllocDefault));
+  CALS_CUDA_TRY(cudaEventCreateWithFlags(&e->st_upload_ev, cudaEventDisableTiming));
   CALS_CUDA_TRY(cudaHostGetDevicePointer(&e->d_done_alias, e->h_done, 0));
 
   // constant tables
@@ -1002,6 +1010,27 @@ static int engine_create(Tensor* t, int capacity, int n_models, const int* ranks
   return kOk;
 }
 
+// Per-model run state to its initial values (driver.py:56-67): status,
+// iteration count, failure / fresh flags 0, retirement order -1, f_prev =
+// -inf, error = +inf, fit = -inf.
+__global__ void engine_reset_kernel(const EngState h, int nm) {
+  for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < nm; k += gridDim.x * blockDim.x) {
+    h.status[k] = 0;
+    h.iters[k] = 0;
+    h.failed[k] = 0;
+    h.fresh[k] = 0;
+    if (h.has_snap) h.has_snap[k] = 0;
+    h.retire_seq[k] = -1;
+    h.f_prev[k] = -INFINITY;
+    h.err[k] = INFINITY;
+    h.fit[k] = -INFINITY;
+  }
+}
+
+// Stream-ordered, no host synchronisation: the state goes up from a
+// page-locked copy (the previous upload from it has completed -- every run
+// ends with a stream sync, and the event guards the step-wise API), the
+// per-model arrays are reset by one kernel.
 static int engine_reset(Engine* e, double tol, int max_iterations, double sqnorm,
                         cudaStream_t stream) {
   EngState& h = e->h_st;
@@ -1010,22 +1039,48 @@ static int engine_reset(Engine* e, double tol, int max_iterations, double sqnorm
   h.tol = tol;
   h.max_iterations = max_iterations;
   h.sqnorm = sqnorm;
-  const size_t nm = std::max(1, e->n_models);
-  CALS_CUDA_TRY(cudaMemsetAsync(h.status, 0, nm * 4, stream));
-  CALS_CUDA_TRY(cudaMemsetAsync(h.iters, 0, nm * 4, stream));
-  CALS_CUDA_TRY(cudaMemsetAsync(h.failed, 0, nm * 4, stream));
-  CALS_CUDA_TRY(cudaMemsetAsync(h.fresh, 0, nm * 4, stream));
-  if (h.has_snap) CALS_CUDA_TRY(cudaMemsetAsync(h.has_snap, 0, nm * 4, stream));
-  CALS_CUDA_TRY(cudaMemsetAsync(h.retire_seq, 0xff, nm * 4, stream));
-  std::vector<double> minf(nm, -INFINITY), pinf(nm, INFINITY);
-  // f_prev = -inf, err = +inf, fit = -inf (driver.py:56-67)
-  CALS_CUDA_TRY(cudaMemcpyAsync(h.f_prev, minf.data(), nm * 8, cudaMemcpyHostToDevice, stream));
-  CALS_CUDA_TRY(cudaMemcpyAsync(h.err, pinf.data(), nm * 8, cudaMemcpyHostToDevice, stream));
-  CALS_CUDA_TRY(cudaMemcpyAsync(h.fit, minf.data(), nm * 8, cudaMemcpyHostToDevice, stream));
-  CALS_CUDA_TRY(cudaMemcpyAsync(e->d_st, &h, sizeof(EngState), cudaMemcpyHostToDevice, stream));
-  CALS_CUDA_TRY(cudaStreamSynchronize(stream));  // the host vectors above are stack-owned
-  *e->h_done = 0;
+  const int nm = std::max(1, e->n_models);
+  CALS_CUDA_TRY(cudaEventSynchronize(e->st_upload_ev));
+  *e->h_st_pinned = h;
+  CALS_CUDA_TRY(cudaMemcpyAsync(e->d_st, e->h_st_pinned, sizeof(EngState), cudaMemcpyHostToDevice,
+                                stream));
+  CALS_CUDA_TRY(cudaEventRecord(e->st_upload_ev, stream));
+  engine_reset_kernel<<<std::max(1, std::min((nm + 255) / 256, 148)), 256, 0, stream>>>(h, nm);
+  CALS_CUDA_TRY(cudaGetLastError());
+  e->h_done[1] = 0;
+  *(volatile int*)e->h_done = 0;
   return kOk;
+}
+
+// Driver iterations a run takes when no model can stop early (tol <= 0: every
+// admitted model runs exactly max_iterations): the FIFO admission with
+// head-of-line blocking (plan kernel) replayed on the host.  Failures can only
+// shorten the run (the extra iterations are no-ops on the device).
+static long long fixed_iteration_count(const Engine* e, int max_iterations) {
+  std::vector<std::pair<int, int>> active;  // (rank, iterations left)
+  int head = 0;
+  long long width = 0, graphs = 0;
+  auto admit = [&] {
+    while (head < e->n_models && width + e->ranks[head] <= e->capacity) {
+      active.push_back({e->ranks[head], max_iterations});
+      width += e->ranks[head++];
+    }
+  };
+  admit();
+  while (!active.empty()) {
+    ++graphs;
+    std::vector<std::pair<int, int>> keep;
+    for (auto& a : active) {
+      if (--a.second > 0)
+        keep.push_back(a);
+      else
+        width -= a.first;
+    }
+    active.swap(keep);
+    admit();
+    if (active.empty() && head < e->n_models) return 0;  // blocked: let the device decide
+  }
+  return graphs;
 }
 
 // M_n -> Mout for the current layout (dimension-tree aware).
@@ -1262,6 +1317,9 @@ static int engine_run(Engine* e, double tol, int max_iterations, double sqnorm, 
     rc = engine_capture(e, stream);
     if (rc) return rc;
   }
+  // tol <= 0: the iteration count is known, so the graphs go out back to back
+  // (no completion polling, no trailing no-op iterations)
+  const long long exact = (use_graph && tol <= 0.0) ? fixed_iteration_count(e, max_iterations) : 0;
   const int kLook = 3;
   cudaEvent_t ev[kLook];
   for (int i = 0; i < kLook; ++i)
@@ -1284,6 +1342,17 @@ static int engine_run(Engine* e, double tol, int max_iterations, double sqnorm, 
     }
     cudaEventRecord(ev[launched % kLook], stream);
     ++launched;
+    if (launched < exact) continue;
+    if (launched == exact) {
+      cudaError_t ce = cudaStreamSynchronize(stream);
+      if (ce != cudaSuccess) {
+        set_error(std::string("engine iteration failed: ") + cudaGetErrorString(ce));
+        result = kErrCuda;
+        break;
+      }
+      if (*(volatile int*)e->h_done) break;
+      continue;  // not done (should not happen): poll as for tol > 0
+    }
     if (launched >= kLook) {
       cudaError_t ce = cudaEventSynchronize(ev[(launched - kLook) % kLook]);
       if (ce != cudaSuccess) {
@@ -1299,8 +1368,7 @@ static int engine_run(Engine* e, double tol, int max_iterations, double sqnorm, 
   if (result) return result;
   CALS_CUDA_TRY(ce);
   CALS_CHECK(*(volatile int*)e->h_done, kErrInvalid, "engine did not terminate");
-  int plans = 0;
-  CALS_CUDA_TRY(cudaMemcpy(&plans, &e->d_st->plans_done, 4, cudaMemcpyDeviceToHost));
+  const int plans = ((volatile int*)e->h_done)[1];
   e->last_iterations = plans - 1;
   if (iterations_out) *iterations_out = plans - 1;
   return kOk;
@@ -1643,6 +1711,8 @@ int cals_engine_begin(cals_engine* e, double tol, int max_iterations, double sqn
   CALS_CHECK(!g->h_st.ls_enabled, kErrUnsupported,
              "line search is not supported by the step-wise (sharded) driver");
   cudaStream_t s = (cudaStream_t)stream;
+  // the previous step-wise run may still be in flight on this stream
+  CALS_CUDA_TRY(cudaStreamSynchronize(s));
   int rc = engine_reset(g, tol, max_iterations, sqnorm, s);
   if (rc) return rc;
   if (g->n_models == 0) {
