@@ -466,7 +466,7 @@ static UpdateKernel update_kernel_for(int max_rank, int* rb) {
 }
 
 // -------------------------------------------------------------------- plan --
-// One warp: retire (registry order), compact survivors, admit FIFO with
+// One block: retire (registry order), compact survivors, admit FIFO with
 // head-of-line blocking (driver.py:198-208, 274-276; multimatrix.py:103-158).
 // block-wide inclusive scan of one int per thread (blockDim.x = kPlanThreads)
 constexpr int kPlanThreads = 1024;
@@ -566,29 +566,56 @@ __global__ void __launch_bounds__(kPlanThreads, 1) engine_plan_kernel(EngState* 
     }
     __syncthreads();
   }
-  if (threadIdx.x == 0) {
-    int new_w = s_new_w, new_n = s_new_n, moves = s_moves, pre = s_pre;
-    int head = st->queue_head;
-    while (head < st->n_models && new_w + st->rank[head] <= st->capacity) {
-      const int k = head++;
+  // FIFO admission with head-of-line blocking (driver.py:199-208,
+  // multimatrix.py:143-158), kPlanThreads queued models per round: the
+  // admitted models are the prefix whose rank prefix sum still fits, so a
+  // block scan places them all at once (same slots, offsets and move list as
+  // admitting one at a time).
+  __shared__ int s_head, s_more;
+  if (threadIdx.x == 0) s_head = st->queue_head;
+  __syncthreads();
+  for (;;) {
+    const int head = s_head, new_w = s_new_w, new_n = s_new_n, moves = s_moves, pre = s_pre;
+    if (head >= st->n_models) break;  // block-uniform
+    const int k = head + threadIdx.x;
+    const bool valid = k < st->n_models;
+    const int rk = valid ? st->rank[k] : 0;
+    int tot_r, n_adm;
+    const int incl = plan_scan(rk, wtot, &tot_r);
+    const bool adm = valid && (long long)new_w + incl <= (long long)st->capacity;
+    plan_scan(adm ? 1 : 0, wtot, &n_adm);
+    if (adm) {
+      const int off = new_w + incl - rk;  // threadIdx.x = index in the admitted prefix
       st->status[k] = kActive;
       st->fresh[k] = 1;
       if (st->has_snap) st->has_snap[k] = 0;
       st->t_admit[k] = now;
-      st->slot_model[new_n] = k;
-      st->slot_off[new_n] = new_w;
-      st->slot_info[new_n] = make_int4(k, st->rank[k], new_w, (int)st->gram_off[k]);
-      st->mv_kind[moves] = kMoveAdmit;
-      st->mv_model[moves] = k;
-      st->mv_src[moves] = 0;
-      st->mv_dst[moves] = new_w;
-      st->mv_len[moves] = st->rank[k];
-      st->mv_pre[moves] = pre;
-      pre += st->rank[k];
-      ++moves;
-      ++new_n;
-      new_w += st->rank[k];
+      st->slot_model[new_n + threadIdx.x] = k;
+      st->slot_off[new_n + threadIdx.x] = off;
+      st->slot_info[new_n + threadIdx.x] = make_int4(k, rk, off, (int)st->gram_off[k]);
+      const int mi = moves + threadIdx.x;
+      st->mv_kind[mi] = kMoveAdmit;
+      st->mv_model[mi] = k;
+      st->mv_src[mi] = 0;
+      st->mv_dst[mi] = off;
+      st->mv_len[mi] = rk;
+      st->mv_pre[mi] = pre + incl - rk;
+      if ((int)threadIdx.x == n_adm - 1) {  // last admitted: carries
+        s_new_w = new_w + incl;
+        s_pre = pre + incl;
+      }
     }
+    if (threadIdx.x == 0) {
+      s_head = head + n_adm;
+      s_new_n = new_n + n_adm;
+      s_moves = moves + n_adm;
+      s_more = n_adm == kPlanThreads;
+    }
+    __syncthreads();
+    if (!s_more) break;
+  }
+  if (threadIdx.x == 0) {
+    const int new_w = s_new_w, new_n = s_new_n, moves = s_moves, pre = s_pre, head = s_head;
     st->old_width = st->width;
     st->move_elems = pre;
     st->n_moves = moves;
