@@ -179,7 +179,16 @@ int plan_splits(const ModePlan& view) {
   }();
   ModePlan p = view;
   p.S = (int)std::max<long long>(1, std::min<long long>(p.Dq, env_splits > 0 ? env_splits : 32));
-  if (env_splits <= 0 && ozaki_eligible(p)) p.S = ozaki_refine_splits(p);
+  if (env_splits <= 0) {
+    if (ozaki_eligible(p)) {
+      p.S = ozaki_refine_splits(p);
+    } else if (p.Dq < 64) {
+      // few slabs: ~2 per split can make the view INT8-eligible
+      ModePlan q = p;
+      q.S = (int)((p.Dq + 1) / 2);
+      if (q.S < p.S && ozaki_eligible(q)) p.S = q.S;
+    }
+  }
   return p.S;
 }
 

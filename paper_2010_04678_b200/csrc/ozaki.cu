@@ -184,8 +184,11 @@ bool ozaki_eligible(const ModePlan& p) {
   const double m_fill = double(p.M) / double((p.M + BNM - 1) / BNM * BNM);
   const double k_fill = double(p.Dp) / double(kp_of(p.Dp));
   // >= 3 slabs per split: the per-unit pipeline fill and the per-slab
-  // epilogue must amortise over enough tensor-core work
-  return p.Dp >= 128 && m_fill * k_fill >= 0.6 && p.Dq >= 3LL * p.S;
+  // epilogue must amortise over enough tensor-core work; views with few slabs
+  // (Dq < 64, e.g. the EEM's 21) take ~2 per split instead (plan_splits
+  // picks S = ceil(Dq / 2) for them; c3: 11 splits, 1.09x over DMMA)
+  const bool slabs_ok = p.Dq >= 3LL * p.S || (p.Dq < 64 && 2LL * p.S <= p.Dq + 1);
+  return p.Dp >= 128 && m_fill * k_fill >= 0.6 && slabs_ok;
 }
 
 // m tiling (see Args): full 64-row tiles plus, when the M % 64 leftover rows
