@@ -114,28 +114,28 @@ __global__ void oz_slice_cols_kernel(const double* __restrict__ lo, long long ld
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const int c = c0 + lane;
   {
-    // 8 independent loads in flight per thread (a rolled loop waits one L2
-    // round trip per row: ~11 us at Dp = 250); max is order independent
-    double m8[8] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
+    // One pass over the column block: up to 32 loads in flight per thread
+    // (a rolled loop waits one L2 round trip per row), the column max (order
+    // independent) and, for the rows of this block's p-chunk, the tile.
+    for (int pp = w; pp < 32; pp += 8) tile[pp][lane] = 0.0;
+    double mx = 0.0;
     if (c < W) {
-      int p = w;
-      for (; p + 56 < Dp; p += 64) {
-        double v[8];
+      for (int pb = w; pb < Dp; pb += 8 * 32) {
+        double v[32];
 #pragma unroll
-        for (int u = 0; u < 8; ++u) v[u] = lo[(long long)(p + 8 * u) * ld + c];
+        for (int u = 0; u < 32; ++u) {
+          const int p = pb + 8 * u;
+          v[u] = p < Dp ? lo[(long long)p * ld + c] : 0.0;
+        }
 #pragma unroll
-        for (int u = 0; u < 8; ++u) m8[u] = fmax(m8[u], abs_or_inf(v[u]));
+        for (int u = 0; u < 32; ++u) {
+          const int p = pb + 8 * u;
+          mx = fmax(mx, abs_or_inf(v[u]));
+          if (p >= p0 && p < p0 + 32 && p < Dp) tile[p - p0][lane] = v[u];
+        }
       }
-      for (; p < Dp; p += 8) m8[0] = fmax(m8[0], abs_or_inf(lo[(long long)p * ld + c]));
     }
-    double mx = m8[0];
-#pragma unroll
-    for (int u = 1; u < 8; ++u) mx = fmax(mx, m8[u]);
     red[w][lane] = mx;
-  }
-  for (int pp = w; pp < 32; pp += 8) {
-    const int p = p0 + pp;
-    tile[pp][lane] = (c < W && p < Dp) ? lo[(long long)p * ld + c] : 0.0;
   }
   __syncthreads();
   if (w == 0) {
