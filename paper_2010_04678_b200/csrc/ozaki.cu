@@ -157,6 +157,60 @@ __global__ void oz_slice_cols_kernel(const double* __restrict__ lo, long long ld
   }
 }
 
+// Short contractions (Kp <= 256): one block per 32 columns does the whole
+// column block -- one pass of loads (<= 32 per thread, all in flight) into a
+// shared-memory tile, the column max from the same values, then every
+// (column, p) element sliced -- instead of Kp/32 blocks that each re-read the
+// full columns for the max.  Same slices and exponents as
+// oz_slice_cols_kernel.
+constexpr int kColsAllMaxKp = 256;
+__global__ void __launch_bounds__(256) oz_slice_cols_all_kernel(
+    const double* __restrict__ lo, long long ld, int Dp, int Kp, const int* width_ptr, int width,
+    long long cap_pad, uint8_t* __restrict__ ls, int* __restrict__ cex, int* __restrict__ queue) {
+  extern __shared__ double ctile[];  // [Kp][33]
+  __shared__ double red[8][33];
+  __shared__ int ex[32];
+  if (blockIdx.x == 0 && threadIdx.x == 0) *queue = 0;
+  const int W = width_ptr ? *width_ptr : width;
+  const int c0 = blockIdx.x * 32;
+  if (c0 >= W) return;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int c = c0 + lane;
+  double v[kColsAllMaxKp / 8];
+#pragma unroll
+  for (int u = 0; u < kColsAllMaxKp / 8; ++u) {
+    const int p = w + 8 * u;
+    v[u] = (c < W && p < Dp) ? lo[(long long)p * ld + c] : 0.0;
+  }
+  double mx = 0.0;
+#pragma unroll
+  for (int u = 0; u < kColsAllMaxKp / 8; ++u) {
+    const int p = w + 8 * u;
+    mx = fmax(mx, abs_or_inf(v[u]));
+    if (p < Kp) ctile[p * 33 + lane] = v[u];
+  }
+  red[w][lane] = mx;
+  __syncthreads();
+  if (w == 0) {
+    double m = red[0][lane];
+#pragma unroll
+    for (int k = 1; k < 8; ++k) m = fmax(m, red[k][lane]);
+    const int e = scale_exp_checked(m);
+    ex[lane] = e;
+    if (c < W) cex[c] = e;
+  }
+  __syncthreads();
+  const size_t slice_stride = size_t(cap_pad) * size_t(Kp);
+  for (int idx = threadIdx.x; idx < 32 * Kp; idx += blockDim.x) {
+    const int cc = idx / Kp, p = idx - cc * Kp;  // consecutive threads: consecutive p
+    uint8_t sl[kSlices];
+    slice7(ctile[p * 33 + cc], ex[cc], sl);
+    uint8_t* dst = ls + size_t(c0 + cc) * size_t(Kp) + p;
+#pragma unroll
+    for (int k = 0; k < kSlices; ++k) dst[k * slice_stride] = sl[k];
+  }
+}
+
 static int view_strides(const Tensor& t, const ModePlan& p, long long& sm, long long& sp,
                         long long& sq) {
   const long long s0 = 1, s1 = p.D[0], s2 = p.D[0] * p.D[1];
@@ -391,10 +445,28 @@ int launch_contraction_ozaki(Tensor& t, const ModePlan& p, int key, const double
   int* queue = cex + cap_pad;  // inside the cap_pad * 8 bytes reserved after the slices
   const int sms = sm_count(t.device);
 
-  oz_slice_cols_kernel<<<dim3((unsigned)((cap + 31) / 32), (unsigned)(o.Kp / 32)), 256, 0,
-                         stream>>>(
-      lo, lo_ld, (int)std::min<long long>(lrows, p.Dp), (int)o.Kp, width_ptr, width, cap_pad, ls,
-      cex, queue);
+  // the one-block-per-column-block kernel wins when there are enough column
+  // blocks to fill the GPU (c2: 66 -> 10.6 vs 12.7 us); narrow pools (c3's
+  // 10) keep the p-chunked grid (9.0 vs 11.4 us)
+  if (o.Kp <= kColsAllMaxKp && (cap + 31) / 32 >= 32) {
+    const size_t smem = size_t(o.Kp) * 33 * 8;
+    static std::once_flag once;
+    static cudaError_t attr = cudaSuccess;
+    std::call_once(once, [] {
+      attr = cudaFuncSetAttribute(oz_slice_cols_all_kernel,
+                                  cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  kColsAllMaxKp * 33 * 8);
+    });
+    CALS_CUDA_TRY(attr);
+    oz_slice_cols_all_kernel<<<(unsigned)((cap + 31) / 32), 256, smem, stream>>>(
+        lo, lo_ld, (int)std::min<long long>(lrows, p.Dp), (int)o.Kp, width_ptr, width, cap_pad,
+        ls, cex, queue);
+  } else {
+    oz_slice_cols_kernel<<<dim3((unsigned)((cap + 31) / 32), (unsigned)(o.Kp / 32)), 256, 0,
+                           stream>>>(
+        lo, lo_ld, (int)std::min<long long>(lrows, p.Dp), (int)o.Kp, width_ptr, width, cap_pad,
+        ls, cex, queue);
+  }
   CALS_CUDA_TRY(cudaGetLastError());
 
   CUtensorMap mapL;
