@@ -115,6 +115,12 @@ int cals_engine_run(cals_engine* e, double tol, int max_iterations, double sqnor
 int cals_engine_results(cals_engine* e, double* pool, int32_t* status, int32_t* iterations,
                         double* error, double* fit, int32_t* retire_seq, double* seconds_active,
                         double* lambdas, void* stream);
+/* Stream-ordered copy of the retired models' factors (the pool: per model,
+ * per mode, the Fortran (I_n, R_k) block -- the reference's copy-out on
+ * retirement, multimatrix.py:97-101) into host memory, without waiting: the
+ * caller synchronises the stream before reading it (run() builds the
+ * returned Model objects while the copy is in flight). */
+int cals_engine_pool_download(cals_engine* e, double* host_pool, void* stream);
 /* One record per driver iteration (driver.py:278-284 SegmentTrace meta). */
 int cals_engine_trace(cals_engine* e, int32_t* widths, int32_t* n_active, double* seconds,
                       int capacity, int* count);

@@ -52,6 +52,7 @@ SIGNATURES = {
     "cals_engine_results": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
                                       C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
                                       C.c_void_p]),
+    "cals_engine_pool_download": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p]),
     "cals_engine_trace": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int,
                                     c_int_p]),
     "cals_engine_variant": (C.c_int, [C.c_void_p, C.c_int, c_int_p, c_int_p, c_int_p, c_int_p]),

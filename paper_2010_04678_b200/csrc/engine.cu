@@ -1578,6 +1578,15 @@ int cals_engine_run(cals_engine* e, double tol, int max_iterations, double sqnor
   return rc;
 }
 
+int cals_engine_pool_download(cals_engine* e, double* host_pool, void* stream) {
+  CALS_CHECK(e && host_pool, kErrInvalid, "null engine or buffer");
+  Engine* g = e->e;
+  if (g->n_models == 0 || g->pool_elems == 0) return kOk;
+  CALS_CUDA_TRY(cudaMemcpyAsync(host_pool, g->h_st.pool, size_t(g->pool_elems) * 8,
+                                cudaMemcpyDeviceToHost, (cudaStream_t)stream));
+  return kOk;
+}
+
 int cals_engine_results(cals_engine* e, double* pool, int32_t* status, int32_t* iterations,
                         double* error, double* fit, int32_t* retire_seq, double* seconds_active,
                         double* lambdas, void* stream) {

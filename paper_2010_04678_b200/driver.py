@@ -169,7 +169,10 @@ def _run_fused(t: DenseTensor, queue: list[Model], cfg: ConvergenceConfig, r_sta
         # host allocator -> no cudaHostAlloc per run) that the returned
         # factors view directly: no host-side copy
         pool_t = torch.empty(max(eng.pool_elems, 1), dtype=torch.float64, pin_memory=True)
-        res = eng.results(pool_out=pool_t.numpy())
+        res = eng.results(with_pool=False)
+        # the factor pool comes down while the Model objects are built below
+        # (they are views into it); the stream is synchronised before return
+        eng.pool_download(pool_t.numpy())
         warned = eng.nnls_warnings() if nonneg else None
         wall = time.perf_counter() - tic
         records = eng.trace() if (trace is not None and not label_per_model) else None
@@ -179,7 +182,6 @@ def _run_fused(t: DenseTensor, queue: list[Model], cfg: ConvergenceConfig, r_sta
     except BaseException:
         eng.close()
         raise
-    _ENGINES.release(eng)
     if warned is not None and warned.any():
         warnings.warn("active-set search hit its iteration cap", NonConvergedNnlsWarning,
                       stacklevel=3)
@@ -188,21 +190,27 @@ def _run_fused(t: DenseTensor, queue: list[Model], cfg: ConvergenceConfig, r_sta
                 upload_wait_s=tic - t3, device_loop_s=t4 - tic, results_download_s=t5 - t4)
     for m in queue:
         m.status = ModelStatus.ACTIVE
-    pool = res.pool
+    pool = pool_t.numpy()
     order = np.argsort(res.retire_seq, kind="stable").tolist()
     lam_off = np.concatenate([[0], np.cumsum(ranks)]).tolist()
     status, err, fit = res.status.tolist(), res.error.tolist(), res.fit.tolist()
     iters, secs = res.iterations.tolist(), res.seconds_active.tolist()
     lam = res.lambdas
     out = []
-    for k in order:
-        src = queue[k]
-        meta = dict(src.meta)
-        meta["lambdas"] = lam[lam_off[k]:lam_off[k + 1]]
-        out.append(Model._from_engine(id=src.id, rank=src.rank, factors=eng.unpack(pool, k),
-                                      error=err[k], fit=fit[k], iterations_done=iters[k],
-                                      status=STATUS_FROM_CODE[status[k]],
-                                      seconds_active=secs[k], meta=meta))
+    try:
+        for k in order:
+            src = queue[k]
+            meta = dict(src.meta)
+            meta["lambdas"] = lam[lam_off[k]:lam_off[k + 1]]
+            out.append(Model._from_engine(id=src.id, rank=src.rank, factors=eng.unpack(pool, k),
+                                          error=err[k], fit=fit[k], iterations_done=iters[k],
+                                          status=STATUS_FROM_CODE[status[k]],
+                                          seconds_active=secs[k], meta=meta))
+    finally:
+        # the factor views are valid once the pool download has landed; only
+        # then may another run reuse the engine (and its device pool)
+        torch.cuda.current_stream().synchronize()
+        _ENGINES.release(eng)
     prof["build_models_s"] = time.perf_counter() - t5
     if trace is not None:
         if label_per_model:

@@ -154,6 +154,14 @@ class CalsEngine:
                      ptr(err), ptr(fit), ptr(seq), ptr(secs), ptr(lam), s)
         return EngineResults(pool, status, iters, err, fit, seq, secs, lam)
 
+    def pool_download(self, pool_out: np.ndarray, stream=None) -> None:
+        """Enqueue the pool's device-to-host copy into ``pool_out`` (page-locked)
+        without waiting; synchronise the stream before reading it."""
+        import torch
+
+        s = stream if stream is not None else torch.cuda.current_stream().cuda_stream
+        _native.call("cals_engine_pool_download", self.handle, pool_out.ctypes.data, s)
+
     def trace(self):
         cap = self.trace_capacity
         w = np.empty(cap, np.int32)
