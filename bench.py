@@ -298,11 +298,12 @@ def main_gpu(args) -> None:
     # launches per step (matches the ncu launch list of tools/ncu_engine.py):
     # per driver iteration, order 3 with the dimension tree: two tensor-core
     # contractions (+ split reduce, + the per-call Lo slicing on the INT8
-    # path), one partial TTV, three updates, plan + move; initial plan + move
+    # path), one partial TTV, three updates, plan + move; per run the state
+    # reset kernel and the initial plan + move
     k2, o2 = C.c_int32(), C.c_double()
     _native.call("cals_mttkrp_kernel_info", dev_t.handle, 2, r_star, C.byref(k2), C.byref(o2))
     per_contraction = 2 + (1 if k2.value == 1 else 0)
-    gpu_launches = int(round(np.mean(iters_run))) * (2 * per_contraction + 1 + 3 + 2) + 2
+    gpu_launches = int(round(np.mean(iters_run))) * (2 * per_contraction + 1 + 3 + 2) + 3
 
     # ---- e2e through the public API with host buffers
     from paper_2010_04678_b200.driver import LAST_RUN_PROFILE
