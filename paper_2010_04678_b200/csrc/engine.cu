@@ -52,6 +52,10 @@ struct EngState {
   // kernel next to slot_model / slot_off, read by the update kernel in one
   // load (no slot -> model -> rank / offset dependent round trips)
   int4* slot_info;
+  // models that left the active state since the last plan (decide_model);
+  // zero -> the next plan is a no-op (no retirement frees width, so no
+  // admission is possible either)
+  int* changed;
   // move plan
   int* mv_kind;
   int* mv_model;
@@ -112,23 +116,28 @@ __device__ inline void decide_model(EngState* st, int k, double e) {
     st->err[k] = nan("");
     st->fit[k] = -INFINITY;
     st->status[k] = kFailed;
+    atomicAdd(st->changed, 1);
     return;
   }
   if (!isfinite(e)) {
     st->err[k] = e;
     st->fit[k] = -INFINITY;
     st->status[k] = kFailed;
+    atomicAdd(st->changed, 1);
     return;
   }
   const double f = 1.0 - sqrt(e) / sqrt(st->sqnorm);
   st->err[k] = e;
   st->fit[k] = f;
-  if (st->tol > 0.0 && f - st->f_prev[k] < st->tol)
+  if (st->tol > 0.0 && f - st->f_prev[k] < st->tol) {
     st->status[k] = kConverged;
-  else if (it >= st->max_iterations)
+    atomicAdd(st->changed, 1);
+  } else if (it >= st->max_iterations) {
     st->status[k] = kCap;
-  else
+    atomicAdd(st->changed, 1);
+  } else {
     st->f_prev[k] = f;
+  }
 }
 
 // ------------------------------------------------------------------ update --
@@ -506,6 +515,23 @@ __global__ void __launch_bounds__(kPlanThreads, 1) engine_plan_kernel(EngState* 
   __shared__ int wtot[32];
   __shared__ int s_new_w, s_new_n, s_retired, s_moves, s_pre;
   const unsigned long long now = globaltimer_ns();
+  if (st->plans_done > 0 && *st->changed == 0) {
+    // nothing retired: same slots, no moves, no admission possible; only the
+    // trace record (driver.py:278-284) and the plan count
+    if (threadIdx.x == 0) {
+      const int rec = st->plans_done;
+      st->old_width = st->width;
+      st->move_elems = 0;
+      st->n_moves = 0;
+      if (rec < st->tr_cap) {
+        st->tr_width[rec] = st->width;
+        st->tr_active[rec] = st->n_active;
+        st->tr_time[rec] = now;
+      }
+      st->plans_done = rec + 1;
+    }
+    return;
+  }
   const int n_old = st->n_active;
   if (threadIdx.x == 0) {
     s_new_w = 0;
@@ -630,6 +656,7 @@ __global__ void __launch_bounds__(kPlanThreads, 1) engine_plan_kernel(EngState* 
       st->tr_time[rec] = now;
     }
     st->plans_done = rec + 1;
+    *st->changed = 0;
     if (new_n == 0 && head >= st->n_models) {
       st->done = 1;
       st->host_done[1] = rec + 1;  // plan count, read by the host without a copy
@@ -953,6 +980,7 @@ static int engine_create(Tensor* t, int capacity, int n_models, const int* ranks
   items.push_back({(void**)&h.slot_model, size_t(ms) * 4});
   items.push_back({(void**)&h.slot_off, size_t(ms) * 4});
   items.push_back({(void**)&h.slot_info, size_t(ms) * 16});
+  items.push_back({(void**)&h.changed, 4});
   items.push_back({(void**)&h.mv_kind, size_t(mv) * 4});
   items.push_back({(void**)&h.mv_model, size_t(mv) * 4});
   items.push_back({(void**)&h.mv_src, size_t(mv) * 4});
@@ -1041,6 +1069,7 @@ static int engine_create(Tensor* t, int capacity, int n_models, const int* ranks
 // iteration count, failure / fresh flags 0, retirement order -1, f_prev =
 // -inf, error = +inf, fit = -inf.
 __global__ void engine_reset_kernel(const EngState h, int nm) {
+  if (blockIdx.x == 0 && threadIdx.x == 0) *h.changed = 0;
   for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < nm; k += gridDim.x * blockDim.x) {
     h.status[k] = 0;
     h.iters[k] = 0;
