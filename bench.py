@@ -23,17 +23,20 @@ sweep.
             rate (2*W*prod(dims) per launch, mttkrp.py:72-76) against the live
             DMMA peak (cals_fp64_peak_probe); on the DMMA path the latter only.
   cpu_baseline -- the reference package (baseline/_ref, unmodified) on the
-            host cores: one CALS iteration of the same workload, extrapolated
-            to the 5-iteration sweep.
+            host cores, rank 0 at N=1: a 1-iteration warm-up run, then the
+            full workload's sweep (c2: 200 models x 5 iterations) timed.
 
-Multi-GPU: one process per GPU (torchrun); each rank runs its own c2-sized
-model batch against a replicated tensor (no collective on the data path) ->
-"scaling": "weak".  ``--config c4`` instead splits the fixed 500-model c4
-sweep (500^3) into rank-balanced model batches ("scaling": "strong");
-``--config c3`` runs the converging EEM-shaped sweep with converged-slot
-refill (r_star = 300).
+Multi-GPU: one process per GPU (torchrun), tensor replicated, no collective
+on the data path.  With --gpus N > 1 the default workload is c4: the fixed
+500-model 500^3 sweep split into rank-balanced model batches ("scaling":
+"strong", widths per rank in ``config``).  ``--config c2`` at N > 1 runs
+one c2 batch per rank (weak scaling); ``--config c3`` runs the converging
+EEM-shaped sweep with converged-slot refill (r_star = 300).
 
-``--impl reference`` times the reference CPU implementation instead.
+``--impl reference`` times the reference CPU implementation instead: every
+step one full ``cals.run`` of the same workload on all host cores (c4: a
+rank-balanced tenth of the sweep, scaled by width -- the full c4 sweep is
+~20 TFLOP on the host).
 """
 
 from __future__ import annotations
@@ -51,15 +54,11 @@ import numpy as np
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
-DIMS = (200, 200, 200)
-RANKS = list(range(1, 21))
-PER_RANK = 10
-ITERS = 5
-R_STAR = 2100
 METRIC = "models/sec for full CALS sweep (200^3, 200 models, ranks 1-20 x 10, 5 iterations)"
 
-# BASELINE.json configs usable from bench.py (c2 is the default / headline;
-# c3 and c4 are extra evidence runs: python bench.py --config c4 ...)
+# BASELINE.json configs usable from bench.py.  c2 is the N=1 headline; with
+# --gpus N > 1 the default is c4's fixed 500-model sweep split over the ranks
+# (strong scaling); c3 is the converging refill sweep.
 WORKLOADS = {
     "c2": dict(dims=(200, 200, 200), true_rank=20, ranks=list(range(1, 21)), per_rank=10,
                tol=0.0, iters=5, r_star=2100, shard=False,
@@ -81,14 +80,32 @@ def _env_rank():
             int(os.environ.get("LOCAL_RANK", 0)))
 
 
-def _config(n_gpus: int, extra: dict | None = None) -> dict:
-    c = {"workload": "c2: 200x200x200 dense FP64, 200 CP models (ranks 1..20 x 10), "
-                     "tol=0, 5 iterations per model, r_star=2100",
-         "dims": list(DIMS), "models_per_gpu": len(RANKS) * PER_RANK, "iterations": ITERS,
-         "r_star": R_STAR, "parallelism": f"model-batch x{n_gpus}, tensor replicated",
+def _metric(name: str) -> str:
+    return METRIC if name == "c2" else \
+        f"models/sec for full CALS sweep ({WORKLOADS[name]['desc']})"
+
+
+def _config(name: str, world: int) -> dict:
+    """The ``config`` object -- identical for both arms of the same run."""
+    from paper_2010_04678_b200.parallel import shard_widths
+
+    wl = WORKLOADS[name]
+    ranks = [r for r in wl["ranks"] for _ in range(wl["per_rank"])]
+    c = {"workload": wl["desc"], "dims": list(wl["dims"]),
+         "models_total": len(ranks) * (1 if wl["shard"] else world),
+         "models_per_gpu": len(ranks) if not wl["shard"] else None,
+         "tol": wl["tol"], "max_iterations": wl["iters"],
+         "r_star": wl["r_star"],
+         "parallelism": (f"model-batch x{world} (rank-balanced snake partition of the fixed "
+                         f"sweep), tensor replicated, no collective" if wl["shard"] else
+                         f"model-batch x{world} (every rank its own batch), tensor replicated, "
+                         f"no collective"),
          "l2": "flushed between steps (256 MiB write)"}
-    if extra:
-        c.update(extra)
+    if wl["shard"]:
+        c["widths_per_rank"] = shard_widths(ranks, world)
+        c["models_per_rank"] = [len(s) for s in __import__(
+            "paper_2010_04678_b200.parallel", fromlist=["x"]).snake_partition(ranks, world)]
+        c["r_star"] = "width of the rank's batch"
     return c
 
 
@@ -162,59 +179,126 @@ def _reference_module():
     return None, "port"
 
 
-def cpu_sample(threads: int) -> dict:
-    """One CALS driver iteration of the c2 workload on the host cores."""
-    ref, kind = _reference_module()
-    if ref is not None:
-        from cals.als import ConvergenceConfig
-        from cals.driver import ExecutionMode, run
-        from cals.io import build_models, generate_synthetic
+class _CpuWorkload:
+    """The workload's inputs for the host-side arm: the unmodified reference
+    (``baseline/_ref``) when installed, else the oracle port."""
 
-        t = generate_synthetic(DIMS, 20, 0.1, seed=0)
-        models = build_models(DIMS, RANKS, PER_RANK, seed=1)
-        tic = time.perf_counter()
-        run(t, models, ConvergenceConfig(tol=0.0, max_iterations=1), mode=ExecutionMode.CALS,
-            r_star=R_STAR, threads=threads)
-        sec = time.perf_counter() - tic
-    else:
+    def __init__(self, name: str, world: int = 1):
+        from paper_2010_04678_b200.parallel import snake_partition
+
+        self.name = name
+        self.wl = wl = WORKLOADS[name]
+        self.ref, self.kind = _reference_module()
+        if self.ref is not None:
+            from cals.io import build_models, generate_synthetic
+
+            self.t = generate_synthetic(wl["dims"], wl["true_rank"], 0.1, seed=0)
+            every = build_models(wl["dims"], wl["ranks"], wl["per_rank"], seed=1)
+        else:
+            from oracle import cals_oracle as O
+
+            self.dims, self.data = O.generate_synthetic(wl["dims"], wl["true_rank"], 0.1, seed=0)
+            every = O.build_models(self.dims, wl["ranks"], wl["per_rank"], seed=1)
+        rank_of = (lambda m: m.rank) if self.ref is not None else (lambda m: m[1])
+        self.total_models = len(every)
+        self.total_width = sum(rank_of(m) for m in every)
+        self.sampled = False
+        if wl["shard"]:
+            # c4: the full sweep is ~4 TFLOP per iteration plus a 10.5 GB KRP
+            # workspace on the host -- a step is one tenth of it (shard 0 of a
+            # 10-way rank-balanced snake partition, every model run its full
+            # 5 iterations) and the rate is scaled by the width ratio (MTTKRP
+            # cost is linear in W, mttkrp.py:72-76)
+            part = snake_partition([rank_of(m) for m in every], 10)[0]
+            self.models = [every[i] for i in part]
+            self.sampled = True
+        else:
+            self.models = every
+        self.width = sum(rank_of(m) for m in self.models)
+        self.r_star = wl["r_star"] or self.width
+
+    def fresh_models(self):
+        if self.ref is not None:
+            from cals.model import Model
+
+            return [Model(id=m.id, rank=m.rank, factors=[f.copy() for f in m.factors])
+                    for m in self.models]
+        return [(i, r, [f.copy() for f in fac]) for i, r, fac in self.models]
+
+    def run(self, threads: int, iters: int | None = None) -> float:
+        wl = self.wl
+        iters = wl["iters"] if iters is None else iters
+        models = self.fresh_models()
+        if self.ref is not None:
+            from cals.als import ConvergenceConfig
+            from cals.driver import ExecutionMode, run
+
+            tic = time.perf_counter()
+            run(self.t, models, ConvergenceConfig(tol=wl["tol"], max_iterations=iters),
+                mode=ExecutionMode.CALS, r_star=self.r_star, threads=threads)
+            return time.perf_counter() - tic
         from oracle import cals_oracle as O
 
-        dims, data = O.generate_synthetic(DIMS, 20, 0.1, seed=0)
-        models = O.build_models(dims, RANKS, PER_RANK, seed=1)
         tic = time.perf_counter()
-        O.run_cals(data, dims, models, 0.0, 1, R_STAR)
-        sec = time.perf_counter() - tic
-    n = len(RANKS) * PER_RANK
-    return {"value": n / (sec * ITERS), "unit": "models/s", "cores": threads, "kind": kind,
-            "sample": f"1 of {ITERS} CALS iterations over all {n} models (c2), "
-                      f"{sec:.2f} s, extrapolated x{ITERS}",
-            "seconds_per_iteration": sec}
+        O.run_cals(self.data, self.dims, models, wl["tol"], iters, self.r_star)
+        return time.perf_counter() - tic
+
+    def rate(self, sec: float) -> float:
+        """models/s of the whole workload from one timed step."""
+        if self.sampled:
+            return self.total_models / (sec * self.total_width / self.width)
+        return len(self.models) / sec
+
+    def sample_text(self, n_steps: int, sec: float) -> str:
+        what = (f"{len(self.models)} of {self.total_models} models (rank-balanced 1/10 share, "
+                f"W={self.width} of {self.total_width}), full {self.wl['iters']}-iteration "
+                f"sweep, rate scaled by the width ratio" if self.sampled else
+                f"the full workload ({len(self.models)} models, "
+                f"{'tol ' + str(self.wl['tol']) if self.wl['tol'] > 0 else str(self.wl['iters']) + ' iterations'})")
+        return (f"{self.name}: {what}; reference cals.run(mode=CALS, r_star={self.r_star}); "
+                f"mean of {n_steps} timed run(s) after a 1-iteration warm-up run, "
+                f"{sec:.2f} s per run")
+
+
+def cpu_sample(name: str, threads: int, steps: int = 2) -> dict:
+    """Bounded host-core baseline for the cpu_baseline key (rank 0, N=1)."""
+    w = _CpuWorkload(name)
+    w.run(threads, iters=1)  # warm-up (first touch of the workspaces), as bench.py:191-195
+    secs = [w.run(threads) for _ in range(steps)]
+    sec = float(np.mean(secs))
+    return {"value": w.rate(sec), "unit": "models/s", "cores": threads, "kind": w.kind,
+            "sample": w.sample_text(steps, sec)}
 
 
 def run_reference_arm(args) -> None:
+    """The reference's own CPU implementation, unmodified, through its public
+    ``cals.run`` on all host cores: every step is one full sweep of the same
+    workload (c2: 200 models x 5 iterations), after ``warmup`` untimed ones."""
     rank, world, _ = _env_rank()
     if rank != 0:
         return
+    name = args.config or ("c2" if args.gpus <= 1 else "c4")
     threads = os.cpu_count() or 1
-    try:
-        from threadpoolctl import threadpool_limits
-    except Exception:  # pragma: no cover
-        threadpool_limits = None
-    times = []
-    for i in range(args.warmup + args.steps):
-        s = cpu_sample(threads)
-        if i >= args.warmup:
-            times.append(s["seconds_per_iteration"])
-    sec = float(np.mean(times)) * ITERS
-    n = len(RANKS) * PER_RANK
-    v = n / sec
-    line = {"impl": "reference", "metric": METRIC, "value": v, "unit": "models/s",
+    w = _CpuWorkload(name, world)
+    w.run(threads, iters=1)
+    for _ in range(args.warmup):
+        w.run(threads)
+    secs = [w.run(threads) for _ in range(args.steps)]
+    sec = float(np.mean(secs))
+    v = w.rate(sec)
+    sample = w.sample_text(args.steps, sec)
+    line = {"impl": "reference", "metric": _metric(name), "value": v, "unit": "models/s",
             "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": sec * 1e3, "higher_is_better": True, "scaling": "weak",
-            "vs_baseline": None, "dtype": "f64", "data": "synthetic (generate_synthetic seed 0)",
-            "config": _config(1, {"host": "reference CPU path, all host cores"}),
-            "cpu_baseline": {"value": v, "unit": "models/s", "cores": threads, "kind": s["kind"],
-                             "sample": s["sample"]},
+            "ms_per_step": sec * 1e3, "higher_is_better": True,
+            "scaling": "strong" if WORKLOADS[name]["shard"] else "weak",
+            "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (generate_synthetic noise 0.1 seed 0; build_models seed 1)",
+            "config": _config(name, args.gpus),
+            "host": {"threads": threads, "impl": "reference CPU path (baseline/_ref, unmodified)"
+                     if w.kind == "reference" else "oracle port (reference not installed)",
+                     "step_seconds": [round(x, 4) for x in secs]},
+            "cpu_baseline": {"value": v, "unit": "models/s", "cores": threads, "kind": w.kind,
+                             "sample": sample},
             "e2e": {"value": v, "unit": "models/s", "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
@@ -239,7 +323,8 @@ def main_gpu(args) -> None:
     stream = torch.cuda.current_stream()
     s = stream.cuda_stream
 
-    wl = WORKLOADS[args.config]
+    name = args.config or ("c2" if world <= 1 else "c4")
+    wl = WORKLOADS[name]
     dims = wl["dims"]
     t = cals.generate_synthetic(dims, wl["true_rank"], 0.1, seed=0)
     if wl["shard"]:  # fixed total work split over the ranks (strong scaling)
@@ -382,7 +467,7 @@ def main_gpu(args) -> None:
         roofline = {"bound": "tensor", "achieved": ach, "peak": peak_i8.value, "unit": "TOPS",
                     "frac": ach / peak_i8.value, "traffic": traffic,
                     "kernel": f"mttkrp_ozaki_kernel (INT8 tcgen05, 7x7 Ozaki slices, 28 products) "
-                              f"+ Lo slicing + split reduce (cals_mttkrp), W={W}, {args.config}",
+                              f"+ Lo slicing + split reduce (cals_mttkrp), W={W}, {name}",
                     "achieved_counts": "executed INT8 ops: 2 x 28 slice products x padded "
                                        "M x W x K tiles per slab",
                     "peak_source": "cals_int8_peak_probe: tcgen05.mma kind::i8 M128 N256 K32 on "
@@ -396,39 +481,36 @@ def main_gpu(args) -> None:
         roofline = {"bound": "tensor", "achieved": fp64_eq, "peak": peak.value, "unit": "TFLOP/s",
                     "frac": fp64_eq / peak.value, "traffic": traffic,
                     "kernel": f"mttkrp_dmma_kernel + split_reduce (cals_mttkrp), W={W}, "
-                              f"{args.config} shape",
+                              f"{name} shape",
                     "ms_per_launch_by_mode": per_mode,
                     "peak_source": "cals_fp64_peak_probe: DMMA.8x8x4 all SMs, measured live "
                                    "(MEASURED_PEAKS.json has no FP64 entry)",
                     "flops_per_launch": flops}
 
     it_mean = float(np.mean(iters_run))
-    cfg = {"workload": wl["desc"], "dims": list(dims), "models_total": total_models,
-           "models_this_gpu": n_models, "r_star": r_star,
-           "parallelism": f"model-batch x{world}, tensor replicated, no collective",
-           "l2": "flushed between steps (256 MiB write)",
-           "driver_iterations_per_step": it_mean,
-           "mttkrp_kernels": {f"mode{n}": ("int8-ozaki" if k == 1 else "fp64-dmma")
-                              for n, k in enumerate(kinds)},
-           "tensor_slices": "the INT8 path's tensor slices (a derived format of the immutable "
-                            "tensor) are built once per tensor: outside the timed steps of "
-                            "`value` (tensor resident), inside every step of `e2e` (fresh "
-                            "tensor per run)"}
+    cfg = _config(name, world)
+    details = {"models_this_gpu": n_models, "r_star_this_gpu": r_star,
+               "driver_iterations_per_step": it_mean,
+               "mttkrp_kernels": {f"mode{n}": ("int8-ozaki" if k == 1 else "fp64-dmma")
+                                  for n, k in enumerate(kinds)},
+               "tensor_slices": "the INT8 path's tensor slices (a derived format of the "
+                                "immutable tensor) are built once per tensor: outside the timed "
+                                "steps of `value` (tensor resident), inside every step of `e2e` "
+                                "(fresh tensor per run)"}
     if wl["tol"] <= 0:  # reference flop model (driver.py:124-125) over the sweep
-        cfg["sweep_mttkrp_tflops_reference_model"] = 3 * wl["iters"] * 2 * sum(
-            m.rank for m in models) * float(np.prod(dims)) / (ms_max * 1e-3) / 1e12
-    metric = METRIC if args.config == "c2" else f"models/sec for full CALS sweep ({wl['desc']})"
-    line = {"metric": metric, "value": value, "unit": "models/s", "n_gpus": world,
+        details["sweep_mttkrp_tflops_reference_model"] = 3 * wl["iters"] * 2 * sum(
+            m.rank for m in models) * float(np.prod(dims)) * world / (ms_max * 1e-3) / 1e12
+    line = {"metric": _metric(name), "value": value, "unit": "models/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_max,
             "higher_is_better": True, "scaling": "strong" if wl["shard"] else "weak",
             "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (generate_synthetic noise 0.1 seed 0; build_models seed "
                     + ("1" if wl["shard"] else "1+rank") + ")",
-            "config": cfg, "clocks": clk, "e2e": e2e, "gpu_launches": gpu_launches,
-            "roofline": roofline}
-    if rank == 0 and world == 1 and not args.no_cpu_baseline and args.config == "c2":
-        line["cpu_baseline"] = {k: v for k, v in cpu_sample(os.cpu_count() or 1).items()
-                                if k != "seconds_per_iteration"}
+            "config": cfg, "details": details, "clocks": clk, "e2e": e2e,
+            "gpu_launches": gpu_launches, "roofline": roofline}
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        line["cpu_baseline"] = cpu_sample(name, os.cpu_count() or 1,
+                                          steps=1 if wl["shard"] or wl["tol"] > 0 else 2)
     if rank == 0:
         print(json.dumps(line), flush=True)
     eng.close()
@@ -443,7 +525,8 @@ def main() -> None:
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--config", default="c2", choices=sorted(WORKLOADS))
+    ap.add_argument("--config", default=None, choices=sorted(WORKLOADS),
+                    help="default: c2 at --gpus 1, c4 (strong scaling) at --gpus > 1")
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference_arm(args)

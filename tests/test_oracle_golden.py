@@ -124,3 +124,21 @@ def test_run_other_orders_and_failure():
     f = load("fail_inputs.npz")
     models = [("bad", 2, [f[f"bad_f{n}"] for n in range(3)]), ("good", 2, [f[f"good_f{n}"] for n in range(3)])]
     _check_run("fail", (4, 4, 3), f["data"], models, 0.0, 3, 4)
+
+
+def test_oracle_c2_benchmark_config_matches_reference():
+    """configs[1] as the bench times it (200^3, 200 models, 5 iterations,
+    r_star 2100): the oracle against the reference's own run
+    (run_c2_fixed5.npz, oracle/make_golden_configs.py) -- so the GPU test that
+    compares all 200 models with the oracle is anchored to the reference."""
+    g = load("run_c2_fixed5.npz")
+    dims, data = O.generate_synthetic((200, 200, 200), 20, 0.1, seed=0)
+    models = O.build_models(dims, list(range(1, 21)), 10, seed=1)
+    out = O.run_cals(data, dims, models, 0.0, 5, 2100)
+    assert [r.id for r in out] == [str(s) for s in g["order"]]
+    assert [r.iterations for r in out] == g["iterations"].tolist()
+    for r, f in zip(out, g["fit"]):
+        assert abs(r.fit - f) <= 1e-12
+        if f"{r.id}_f0" in g.files:
+            for n in range(3):
+                assert rel(r.factors[n], g[f"{r.id}_f{n}"]) <= 1e-11, (r.id, n)
