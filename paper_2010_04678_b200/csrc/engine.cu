@@ -1502,7 +1502,17 @@ int cals_mttkrp_kernel_info(cals_tensor* t, int mode, int64_t width, int32_t* ke
   CALS_CHECK(mode >= 0 && mode < t->t->order, kErrInvalid, "mode out of range");
   CALS_CHECK(width >= 1, kErrInvalid, "width must be >= 1");
   const ModePlan& p = t->t->plans[mode];
-  if (ozaki_eligible(p)) {
+  bool int8 = ozaki_eligible(p);
+  if (int8) {
+    // data-dependent part of the choice: the tensor slices are built (once)
+    // and checked -- non-finite entries, scales beyond 2^+-900 and the
+    // dynamic-range guard send the view to the FP64 kernel
+    const int rc = ozaki_prepare(*t->t, p, mode, (cudaStream_t)0, true);
+    if (rc) return rc;
+    std::lock_guard<std::mutex> lk(t->t->mu);
+    int8 = t->t->oz.count(mode) != 0;
+  }
+  if (int8) {
     *kernel = 1;
     *tensor_ops = ozaki_tensor_ops(p, width);
   } else {

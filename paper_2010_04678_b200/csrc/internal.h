@@ -111,6 +111,7 @@ int launch_contraction(Tensor& t, const ModePlan& p, int map_key, const double* 
 // Ozaki-sliced INT8 tensor-core contraction (ozaki.cu) ------------------------
 bool ozaki_enabled();                       // CALS_MTTKRP=dmma disables it
 bool ozaki_eligible(const ModePlan& p);
+bool ozaki_range_guard();                   // CALS_OZ_RANGE_GUARD=0 disables it
 int ozaki_refine_splits(const ModePlan& p);  // shape-only split count for an INT8 view
 size_t ozaki_ws_bytes(const ModePlan& p, long long cap);  // per-call Lo slices
 double ozaki_tensor_ops(const ModePlan& p, long long width);  // INT8 ops per launch

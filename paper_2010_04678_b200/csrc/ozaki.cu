@@ -67,6 +67,15 @@ __global__ void oz_slice_rows_kernel(const double* __restrict__ x, long long sm,
   __syncthreads();
   // ---- pass 2: slices, written p-contiguous (32-byte segments per warp store)
   const size_t slice_stride = size_t(Dq) * size_t(M) * size_t(Kp);
+  // dynamic-range guard: per row, nonzero entries and those below
+  // 2^-kRangeBits of the row maximum (rows r = w, w + 8, w + 16, w + 24)
+  int n_nz[4] = {0, 0, 0, 0}, n_small[4] = {0, 0, 0, 0};
+  double thr[4];
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    const int e = ex[w + 8 * j];
+    thr[j] = (e == kNonFinite) ? 0.0 : ldexp(1.0, e - kRangeBits);
+  }
   for (int p0 = 0; p0 < Kp; p0 += 32) {
     if (mfast) {
       const int m = m0 + lane;
@@ -82,16 +91,42 @@ __global__ void oz_slice_rows_kernel(const double* __restrict__ x, long long sm,
       }
     }
     __syncthreads();
-    for (int r = w; r < 32; r += 8) {
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int r = w + 8 * j;
       const int m = m0 + r;
       if (m >= M) continue;
+      const double v = tile[r][lane];
+      const double a = fabs(v);
+      n_nz[j] += a != 0.0;
+      n_small[j] += a != 0.0 && a < thr[j];
       uint8_t s[kSlices];
-      slice7(tile[r][lane], ex[r], s);
+      slice7(v, ex[r], s);
       uint8_t* dst = xs + (size_t(q) * M + m) * size_t(Kp) + p0 + lane;
 #pragma unroll
       for (int k = 0; k < kSlices; ++k) dst[k * slice_stride] = s[k];
     }
     __syncthreads();
+  }
+  // view-wide dynamic-range census (ozaki_check): nonzero entries, and those
+  // kept with fewer than 55 - kRangeBits bits (below 2^-kRangeBits of their
+  // row maximum)
+  int nz = 0, nsmall = 0;
+#pragma unroll
+  for (int j = 0; j < 4; ++j)
+    if (m0 + w + 8 * j < M) {
+      nz += n_nz[j];
+      nsmall += n_small[j];
+    }
+#pragma unroll
+  for (int o = 16; o; o >>= 1) {
+    nz += __shfl_xor_sync(0xffffffffu, nz, o);
+    nsmall += __shfl_xor_sync(0xffffffffu, nsmall, o);
+  }
+  if (lane == 0 && nz > 0) {
+    unsigned long long* census = reinterpret_cast<unsigned long long*>(out_of_range + 2);
+    atomicAdd(census, (unsigned long long)nsmall);
+    atomicAdd(census + 1, (unsigned long long)nz);
   }
 }
 
@@ -227,6 +262,18 @@ static int view_strides(const Tensor& t, const ModePlan& p, long long& sm, long 
 
 static long long kp_of(long long Dp) { return (Dp + KSTEP - 1) / KSTEP * KSTEP; }
 
+constexpr size_t kFlagBytes = 24;
+
+// Dynamic-range guard of the tensor slices (see oz_slice_rows_kernel);
+// CALS_OZ_RANGE_GUARD=0 disables it (tests of the raw INT8 envelope).
+bool ozaki_range_guard() {
+  static const bool on = [] {
+    const char* env = getenv("CALS_OZ_RANGE_GUARD");
+    return !(env && strcmp(env, "0") == 0);
+  }();
+  return on;
+}
+
 bool ozaki_enabled() {
   static const bool on = [] {
     const char* env = getenv("CALS_MTTKRP");
@@ -315,16 +362,22 @@ size_t ozaki_ws_bytes(const ModePlan& p, long long cap) {
 }
 
 // A view whose slicing found rows beyond 2^+-900 or a non-finite entry is
-// dropped (it stays on DMMA).  The check reads a device flag: done here when
-// `validate`, else deferred to ozaki_validate (so the slicing can overlap
-// host work, e.g. the pool packing of run()).
+// dropped (it stays on DMMA), and so is one where most nonzero entries sit
+// more than 2^kRangeBits below their row maximum (they would keep fewer than
+// 55 - kRangeBits bits; CALS_OZ_RANGE_GUARD=0 keeps such views on INT8).  The
+// check reads the device flag block: done here when `validate`, else deferred
+// to ozaki_validate (so the slicing can overlap host work, e.g. the pool
+// packing of run()).
 static int ozaki_check(Tensor& t, int key, OzSlices& o, cudaStream_t stream, bool* keep) {
-  int h_flag = 0;
-  CALS_CUDA_TRY(cudaMemcpyAsync(&h_flag, o.flag, sizeof(int), cudaMemcpyDeviceToHost, stream));
+  int h[kFlagBytes / 4] = {0};
+  CALS_CUDA_TRY(cudaMemcpyAsync(h, o.flag, kFlagBytes, cudaMemcpyDeviceToHost, stream));
   CALS_CUDA_TRY(cudaStreamSynchronize(stream));
   CALS_CUDA_TRY(cudaFreeAsync(o.flag, stream));
   o.flag = nullptr;
-  *keep = h_flag == 0;
+  unsigned long long census[2];
+  memcpy(census, h + 2, sizeof(census));
+  const bool coarse = ozaki_range_guard() && 2 * census[0] > census[1];
+  *keep = h[0] == 0 && !coarse;
   if (!*keep) {
     cudaFreeAsync(o.xs, stream);
     cudaFreeAsync(o.rex, stream);
@@ -373,8 +426,9 @@ int ozaki_prepare(Tensor& t, const ModePlan& p, int key, cudaStream_t stream, bo
   CALS_CUDA_TRY(cudaMallocAsync(reinterpret_cast<void**>(&o.xs), xs_bytes, stream));
   CALS_CUDA_TRY(cudaMallocAsync(reinterpret_cast<void**>(&o.rex), size_t(p.Dq) * p.M * 4, stream));
   int* flag = nullptr;
-  CALS_CUDA_TRY(cudaMallocAsync(reinterpret_cast<void**>(&flag), sizeof(int), stream));
-  CALS_CUDA_TRY(cudaMemsetAsync(flag, 0, sizeof(int), stream));
+  // [0] out-of-range / non-finite flag, [2..5] two u64 census counters
+  CALS_CUDA_TRY(cudaMallocAsync(reinterpret_cast<void**>(&flag), kFlagBytes, stream));
+  CALS_CUDA_TRY(cudaMemsetAsync(flag, 0, kFlagBytes, stream));
   dim3 grid((unsigned)((p.M + 31) / 32), (unsigned)p.Dq);
   oz_slice_rows_kernel<<<grid, 256, 0, stream>>>(t.data, sm, sp, sq, (int)p.M, (int)p.Dp,
                                                  (int)o.Kp, (int)p.Dq, o.xs, o.rex, flag);

@@ -46,6 +46,9 @@ namespace cals {
 namespace oz {
 
 constexpr int kSlices = 7;
+// Tensor rows whose median nonzero magnitude is below 2^-kRangeBits of the row
+// maximum keep < 55 - kRangeBits bits in most entries: such views stay on DMMA.
+constexpr int kRangeBits = 20;
 constexpr int kGroups = 7;   // g = i + j in [2, 8]
 constexpr int BMC = 128;     // c per tile (MMA M, TMEM lanes)
 constexpr int BNM = 64;      // m per tile (MMA N)

@@ -22,3 +22,14 @@ def test_suites_with_forced_int8_mttkrp():
                         *[os.path.join(HERE, f) for f in SUITES]],
                        env=env, capture_output=True, text=True, timeout=1200, cwd=HERE)
     assert r.returncode == 0, (r.stdout[-4000:], r.stderr[-2000:])
+
+
+def test_int8_envelope_without_range_guard():
+    """The accuracy-envelope suite with the dynamic-range guard off: every
+    view of the spiky / log-uniform / EEM-like data runs on INT8 and must
+    still meet the MTTKRP (1e-12) and sweep (1e-9) bars."""
+    env = dict(os.environ, CALS_OZ_RANGE_GUARD="0")
+    r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-m", "gpu", "-p", "no:cacheprovider",
+                        os.path.join(HERE, "test_gpu_ozaki_envelope.py")],
+                       env=env, capture_output=True, text=True, timeout=1200, cwd=HERE)
+    assert r.returncode == 0, (r.stdout[-4000:], r.stderr[-2000:])
