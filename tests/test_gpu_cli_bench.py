@@ -41,7 +41,7 @@ def test_cli_decompose_end_to_end(tmp_path):
 
 def test_bench_harness_reports(tmp_path):
     import paper_2010_04678_b200 as cals
-    from paper_2010_04678_b200 import benchmarks as bm
+    from paper_2010_04678_b200 import bench as bm
 
     rep = bm.bench_mttkrp_sweep((30, 20, 10), [4, 64], reps=2)
     assert rep["kind"] == "mttkrp_sweep" and len(rep["aggregates"]) == 2
