@@ -149,6 +149,14 @@ int cals_nnls_rows(int rows, int rank, const double* m, int64_t ldm, const doubl
                    uint32_t* active, double* x, int64_t ldx, int32_t* converged, int max_iter,
                    void* stream);
 int cals_engine_nnls_warnings(cals_engine* e, int32_t* flags);
+/* Per model: 1 when a factor update raised in the reference's terms
+ * (update_factor / nnls_update on non-finite input -> ValueError,
+ * als.py:84-85; caught as a numerical failure, driver.py:229-231 for CALS,
+ * driver.py:148-160 _fit_or_fail for SEQUENTIAL / PARALLEL).  The sequential
+ * drivers use it to return the reference's failure record (starting factors,
+ * iterations_done 0, error nan); run_single_als re-raises ValueError.
+ * Blocking copy; call after the run. */
+int cals_engine_update_failures(cals_engine* e, int32_t* flags);
 
 /* Step-wise driving of the same loop (what cals_engine_run replays as a CUDA
  * graph), for host-orchestrated runs that interleave collectives: the

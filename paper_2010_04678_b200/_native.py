@@ -64,6 +64,7 @@ SIGNATURES = {
                                  C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p, C.c_int,
                                  C.c_void_p]),
     "cals_engine_nnls_warnings": (C.c_int, [C.c_void_p, C.c_void_p]),
+    "cals_engine_update_failures": (C.c_int, [C.c_void_p, C.c_void_p]),
     "cals_engine_begin":(C.c_int, [C.c_void_p, C.c_double, C.c_int, C.c_double, C.c_void_p]),
     "cals_engine_enqueue_mttkrp": (C.c_int, [C.c_void_p, C.c_int, C.c_void_p]),
     "cals_engine_enqueue_update": (C.c_int, [C.c_void_p, C.c_int, C.c_void_p]),

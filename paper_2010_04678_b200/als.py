@@ -200,10 +200,14 @@ def run_single_als(t, start, cfg: ConvergenceConfig, ls: LineSearchConfig | None
                    nonneg: bool = False, ws=None, variant_table=None):
     """Fit one instance (als.py:281-356) -- the device-resident driver at K=1,
     which is bitwise identical to that model's columns in a fused run."""
-    from .driver import ExecutionMode, run
+    from .driver import _run_fused
 
     if start.dims != t.dims:
         raise ValueError(f"model dims {start.dims} != tensor dims {t.dims}")
-    (out,) = run(t, [start], cfg, mode=ExecutionMode.CALS, r_star=start.rank, ls=ls,
-                 nonneg=nonneg, variant_table=variant_table)
+    if ls is None:
+        ls = LineSearchConfig()
+    # the starting model is not mutated (status included); an update on
+    # non-finite input raises ValueError as update_factor does (als.py:84-85)
+    (out,) = _run_fused(t, [start], cfg, start.rank, None, label_per_model=True, ls=ls,
+                        nonneg=nonneg, raise_on_update_failure=True)
     return out

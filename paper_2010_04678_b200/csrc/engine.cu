@@ -23,122 +23,14 @@
 #include "mttkrp.cuh"
 #include "update.cuh"
 #include "nnls.cuh"
+#include "engine_state.cuh"
+#include "update2.cuh"
 
 namespace cals {
 constexpr int kNnlsWs = kNnlsP * 32 + 32 + 32 * 32;  // per-warp NNLS scratch (doubles)
 }
 
 namespace cals {
-
-enum Status : int { kPending = 0, kActive = 1, kConverged = 2, kCap = 3, kFailed = 4 };
-enum MoveKind : int { kMoveKeep = 0, kMoveRetire = 1, kMoveAdmit = 2 };
-
-struct EngState {
-  // scalars
-  int order, n_models, capacity, max_slots;
-  int width, n_active, queue_head, n_retired;
-  int plans_done;   // number of plan() calls that did work (trace records)
-  int done;
-  int old_width, n_moves, move_elems;
-  int max_rank;
-  double tol, sqnorm;
-  int max_iterations;
-  long long ld;
-  long long dims[kMaxOrder];
-  // slots
-  int* slot_model;
-  int* slot_off;
-  // per slot {model, rank, column offset, Gramian offset}: written by the plan
-  // kernel next to slot_model / slot_off, read by the update kernel in one
-  // load (no slot -> model -> rank / offset dependent round trips)
-  int4* slot_info;
-  // models that left the active state since the last plan (decide_model);
-  // zero -> the next plan is a no-op (no retirement frees width, so no
-  // admission is possible either)
-  int* changed;
-  // move plan
-  int* mv_kind;
-  int* mv_model;
-  int* mv_src;
-  int* mv_dst;
-  int* mv_len;
-  int* mv_pre;  // exclusive prefix of lengths
-  // per model (const)
-  const int* rank;
-  const long long* pool_off;  // [k * order + n]
-  const long long* gram_off;  // [k]
-  long long gram_stride;
-  // per model (state)
-  int* status;
-  int* iters;
-  int* failed;
-  int* fresh;
-  int* retire_seq;
-  double* f_prev;
-  double* err;
-  double* fit;
-  unsigned long long* t_admit;
-  unsigned long long* t_retire;
-  double* grams;  // [order][gram_stride]
-  double* pool;
-  double* F[kMaxOrder];
-  double* Mout;
-  double* scratch;  // per-block pinv scratch
-  // trace
-  int tr_cap;
-  int* tr_width;
-  int* tr_active;
-  unsigned long long* tr_time;
-  volatile int* host_done;
-  // line search (als.py:127-144, driver.py:250-259,272-273): snapshots S of
-  // the previous iterate, candidates C, their Gramians, per-model flags
-  int ls_enabled;
-  double ls_alpha;  // <= 0: alpha = iteration^(1/3)
-  double* S[kMaxOrder];
-  double* Cb[kMaxOrder];
-  double* cgrams;
-  int* has_snap;
-  int* ls_act;
-  double* e_tmp;
-  // non-negative updates (als.py:185-278): per model, mode and factor row
-  // the active-set bitmask carried between iterations
-  int nonneg;
-  unsigned* nnls_state;
-  const long long* nnls_off;  // [k * order + n]
-  int* nnls_warn;             // a row hit the active-set iteration cap
-};
-
-// Stopping rule for model k with squared error e (driver.py:260-273); the
-// caller has already incremented iters[k].  Thread 0 only.
-__device__ inline void decide_model(EngState* st, int k, double e) {
-  const int it = st->iters[k];
-  if (st->failed[k]) {
-    st->err[k] = nan("");
-    st->fit[k] = -INFINITY;
-    st->status[k] = kFailed;
-    atomicAdd(st->changed, 1);
-    return;
-  }
-  if (!isfinite(e)) {
-    st->err[k] = e;
-    st->fit[k] = -INFINITY;
-    st->status[k] = kFailed;
-    atomicAdd(st->changed, 1);
-    return;
-  }
-  const double f = 1.0 - sqrt(e) / sqrt(st->sqnorm);
-  st->err[k] = e;
-  st->fit[k] = f;
-  if (st->tol > 0.0 && f - st->f_prev[k] < st->tol) {
-    st->status[k] = kConverged;
-    atomicAdd(st->changed, 1);
-  } else if (it >= st->max_iterations) {
-    st->status[k] = kCap;
-    atomicAdd(st->changed, 1);
-  } else {
-    st->f_prev[k] = f;
-  }
-}
 
 // ------------------------------------------------------------------ update --
 // RB > 0: fast path (every rank <= RB, rows in registers, chunked Gram);
@@ -761,6 +653,7 @@ enum Tree : int { kTreeNone = 0, kTreeY = 1, kTreeZ = 2 };
 
 struct Engine {
   Tensor* t = nullptr;
+  int device = 0;  // CUDA device of every allocation below (the tensor's)
   unsigned long long tensor_uid = 0;
   int order = 0, n_models = 0, capacity = 0, max_slots = 0, max_rank = 0;
   long long ld = 0;
@@ -794,6 +687,17 @@ struct Engine {
   int upd_grid = 0, upd_nthr = 0, upd_rb = 0;
   UpdateKernel upd_kernel = nullptr;
   size_t upd_smem = 0, move_smem = 0;
+  // split update (update2.cuh): ranks <= 32, Cholesky / pinv updates.  prep(n)
+  // runs on `side`, forked after the previous mode's solve and joined before
+  // solve(n), i.e. concurrently with the fused MTTKRP of mode n.
+  bool split = false;
+  UpdArgs ua{};
+  PrepKernel prep_kernel = nullptr;
+  SolveKernel solve_kernel = nullptr, solve_last_kernel = nullptr;
+  size_t solve_smem = 0;
+  int nch[kMaxOrder] = {0};
+  cudaStream_t side = nullptr;
+  cudaEvent_t ev_fork[kMaxOrder] = {nullptr}, ev_join[kMaxOrder] = {nullptr};
   int move_grid = 0;
   cudaGraph_t graph = nullptr;
   cudaGraphExec_t exec = nullptr;
@@ -887,6 +791,9 @@ static int setup_tree(Engine* e) {
 
 static int engine_free(Engine* e) {
   if (!e) return kOk;
+  int prev = -1;
+  cudaGetDevice(&prev);
+  if (prev != e->device) cudaSetDevice(e->device);
   if (e->exec) cudaGraphExecDestroy(e->exec);
   if (e->graph) cudaGraphDestroy(e->graph);
   if (e->d_block) cudaFree(e->d_block);
@@ -900,6 +807,12 @@ static int engine_free(Engine* e) {
   if (e->h_st_pinned) cudaFreeHost(e->h_st_pinned);
   if (e->st_upload_ev) cudaEventDestroy(e->st_upload_ev);
   if (e->h_results) cudaFreeHost(e->h_results);
+  for (int n = 0; n < kMaxOrder; ++n) {
+    if (e->ev_fork[n]) cudaEventDestroy(e->ev_fork[n]);
+    if (e->ev_join[n]) cudaEventDestroy(e->ev_join[n]);
+  }
+  if (e->side) cudaStreamDestroy(e->side);
+  if (prev >= 0 && prev != e->device) cudaSetDevice(prev);
   delete e;
   return kOk;
 }
@@ -911,6 +824,7 @@ static int engine_create(Tensor* t, int capacity, int n_models, const int* ranks
   CALS_CHECK(n_models >= 0, kErrInvalid, "n_models must be >= 0");
   std::unique_ptr<Engine> e(new Engine());
   e->t = t;
+  e->device = t->device;
   e->tensor_uid = t->uid;
   e->order = t->order;
   e->n_models = n_models;
@@ -1015,6 +929,20 @@ static int engine_create(Tensor* t, int capacity, int n_models, const int* ranks
   items.push_back({(void**)&h.tr_time, size_t(e->trace_cap) * 8});
   items.push_back({(void**)&e->d_lam, size_t(e->lam_elems) * 8});
   items.push_back({(void**)&e->d_lam_off, nmod * 8});
+  // split update buffers
+  // CALS_SPLIT_UPDATE=0 keeps the one-kernel (block per model) update
+  const char* split_env = getenv("CALS_SPLIT_UPDATE");
+  e->split = rmax <= kFastR && (!split_env || atoi(split_env) != 0);
+  int nch_last = 1;
+  for (int n = 0; n < N; ++n) e->nch[n] = int((t->dims[n] + kSolveRows - 1) / kSolveRows);
+  nch_last = e->nch[N - 1];
+  UpdArgs& ua = e->ua;
+  items.push_back({(void**)&ua.pflag, nmod * 4});
+  items.push_back({(void**)&h.arrive, nmod * 4});
+  items.push_back({(void**)&h.solbad, nmod * 4});
+  items.push_back({(void**)&ua.ubuf, size_t(e->gram_stride) * 8});
+  items.push_back({(void**)&ua.gpart, size_t(e->gram_stride) * nch_last * 8});
+  items.push_back({(void**)&ua.ipart, nmod * nch_last * 8});
   size_t total = 0;
   for (auto& it : items) total = align_up(total, 256) + it.bytes;
   CALS_CUDA_TRY(cudaMalloc(&e->d_block, total));
@@ -1026,6 +954,34 @@ static int engine_create(Tensor* t, int capacity, int n_models, const int* ranks
     off += it.bytes;
   }
   CALS_CUDA_TRY(cudaMalloc(&e->d_st, sizeof(EngState)));
+  // split update: kernel-parameter block (constant bank) of device pointers
+  ua.st = e->d_st;
+  ua.n_active = &e->d_st->n_active;
+  ua.slot_info = h.slot_info;
+  ua.failed = h.failed;
+  ua.fresh = h.fresh;
+  ua.arrive = h.arrive;
+  ua.solbad = h.solbad;
+  ua.grams = h.grams;
+  ua.gram_stride = e->gram_stride;
+  ua.Mout = h.Mout;
+  for (int n = 0; n < N; ++n) {
+    ua.F[n] = h.F[n];
+    ua.dims[n] = t->dims[n];
+  }
+  ua.ld = e->ld;
+  ua.order = N;
+  if (e->split) {
+    split_kernels_for(e->upd_rb, &e->prep_kernel, &e->solve_kernel, &e->solve_last_kernel,
+                      &e->solve_smem);
+    CALS_CUDA_TRY(raise_smem_limit((const void*)e->solve_kernel, e->solve_smem));
+    CALS_CUDA_TRY(raise_smem_limit((const void*)e->solve_last_kernel, e->solve_smem));
+    CALS_CUDA_TRY(cudaStreamCreateWithFlags(&e->side, cudaStreamNonBlocking));
+    for (int n = 0; n < N; ++n) {
+      CALS_CUDA_TRY(cudaEventCreateWithFlags(&e->ev_fork[n], cudaEventDisableTiming));
+      CALS_CUDA_TRY(cudaEventCreateWithFlags(&e->ev_join[n], cudaEventDisableTiming));
+    }
+  }
   CALS_CUDA_TRY(cudaHostAlloc(&e->h_done, 64, cudaHostAllocMapped));
   CALS_CUDA_TRY(cudaHostAlloc(&e->h_st_pinned, sizeof(EngState), cudaHostAllocDefault));
   CALS_CUDA_TRY(cudaEventCreateWithFlags(&e->st_upload_ev, cudaEventDisableTiming));
@@ -1075,6 +1031,8 @@ __global__ void engine_reset_kernel(const EngState h, int nm) {
     h.iters[k] = 0;
     h.failed[k] = 0;
     h.fresh[k] = 0;
+    h.arrive[k] = 0;
+    h.solbad[k] = 0;
     if (h.has_snap) h.has_snap[k] = 0;
     h.retire_seq[k] = -1;
     h.f_prev[k] = -INFINITY;
@@ -1220,10 +1178,29 @@ static int enqueue_line_search(Engine* e, cudaStream_t stream) {
   return kOk;
 }
 
+// Split update of mode n: prep(n) forked onto the side stream before the
+// MTTKRP of mode n is queued (it depends only on what the main stream has
+// done so far), solve(n) after both.
+static int enqueue_split_mode(Engine* e, int n, cudaStream_t stream) {
+  CALS_CUDA_TRY(cudaEventRecord(e->ev_fork[n], stream));
+  CALS_CUDA_TRY(cudaStreamWaitEvent(e->side, e->ev_fork[n], 0));
+  e->prep_kernel<<<e->max_slots, kPrepThreads, 0, e->side>>>(e->ua, n);
+  CALS_CUDA_TRY(cudaGetLastError());
+  CALS_CUDA_TRY(cudaEventRecord(e->ev_join[n], e->side));
+  int rc = enqueue_mode_mttkrp(e, n, stream);
+  if (rc) return rc;
+  CALS_CUDA_TRY(cudaStreamWaitEvent(stream, e->ev_join[n], 0));
+  SolveKernel k = n == e->order - 1 ? e->solve_last_kernel : e->solve_kernel;
+  k<<<e->max_slots * e->nch[n], kSolveRows, e->solve_smem, stream>>>(e->ua, n, e->nch[n]);
+  CALS_CUDA_TRY(cudaGetLastError());
+  return kOk;
+}
+
 static int enqueue_iteration(Engine* e, cudaStream_t stream) {
+  const bool split = e->split && !e->h_st.nonneg;
   for (int n = 0; n < e->order; ++n) {
-    int rc = enqueue_mode_mttkrp(e, n, stream);
-    if (!rc) rc = enqueue_mode_update(e, n, stream);
+    int rc = split ? enqueue_split_mode(e, n, stream) : enqueue_mode_mttkrp(e, n, stream);
+    if (!rc && !split) rc = enqueue_mode_update(e, n, stream);
     if (rc) return rc;
   }
   if (e->h_st.ls_enabled) {
@@ -1442,6 +1419,15 @@ struct cals_engine { Engine* e; };
 
 extern "C" {
 
+#ifdef CALS_UPD_PROFILE
+// profiling builds only (not in the public header): the update kernel's
+// per-(mode, slot) phase stamps of the last launches
+int cals_debug_upd_prof(long long* host, size_t bytes) {
+  CALS_CUDA_TRY(cudaMemcpyFromSymbol(host, g_upd_prof, std::min(bytes, sizeof(g_upd_prof))));
+  return kOk;
+}
+#endif
+
 int cals_abi_version(void) { return CALS_B200_ABI_VERSION; }
 
 const char* cals_last_error(void) { return get_error(); }
@@ -1489,6 +1475,7 @@ int cals_mttkrp(cals_tensor* t, int mode, int width, const double* const* factor
   CALS_CHECK(mode >= 0 && mode < t->t->order, kErrInvalid, "mode out of range");
   CALS_CHECK(width >= 1 && width <= ldf, kErrInvalid, "width must be in [1, ldf]");
   CALS_CHECK(variant < num_variants(), kErrInvalid, "unknown variant");
+  { const int rc_ = check_current_device(*t->t); if (rc_) return rc_; }
   FactorSet fs{};
   for (int n = 0; n < t->t->order; ++n) fs.ptr[n] = factors[n];
   fs.ld = ldf;
@@ -1549,6 +1536,7 @@ size_t cals_update_scratch_bytes(int rank) { return size_t(3 * rank * rank + ran
 int cals_engine_create(cals_tensor* t, int r_star, int n_models, const int32_t* ranks,
                        int trace_capacity, cals_engine** out) {
   CALS_CHECK(t && out, kErrInvalid, "null argument");
+  { const int rc_ = check_current_device(*t->t); if (rc_) return rc_; }
   Engine* e = nullptr;
   int rc = engine_create(t->t, r_star, n_models, ranks, trace_capacity, &e);
   if (rc) return rc;
@@ -1713,6 +1701,9 @@ int cals_engine_set_tensor(cals_engine* e, cals_tensor* t) {
   CALS_CHECK(e && t, kErrInvalid, "null argument");
   Engine* g = e->e;
   CALS_CHECK(t->t->order == g->order, kErrInvalid, "tensor order differs from the engine's");
+  { const int rc_ = check_current_device(*t->t); if (rc_) return rc_; }
+  CALS_CHECK(t->t->device == g->device, kErrInvalid,
+             "tensor lives on another CUDA device than the engine");
   // the previously bound tensor may already be destroyed: compare against the
   // engine's own copy of the dims and the tensor's unique id, never the pointer
   for (int n = 0; n < g->order; ++n)
@@ -1764,6 +1755,15 @@ int cals_engine_nnls_warnings(cals_engine* e, int32_t* flags) {
     return kOk;
   }
   CALS_CUDA_TRY(cudaMemcpy(flags, g->h_st.nnls_warn, size_t(g->n_models) * 4,
+                           cudaMemcpyDeviceToHost));
+  return kOk;
+}
+
+int cals_engine_update_failures(cals_engine* e, int32_t* flags) {
+  CALS_CHECK(e && flags, kErrInvalid, "null argument");
+  Engine* g = e->e;
+  if (g->n_models == 0) return kOk;
+  CALS_CUDA_TRY(cudaMemcpy(flags, g->h_st.failed, size_t(g->n_models) * 4,
                            cudaMemcpyDeviceToHost));
   return kOk;
 }

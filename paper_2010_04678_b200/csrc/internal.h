@@ -66,6 +66,8 @@ struct Tensor {
 int tensor_create(int order, const int64_t* dims, const double* host, const double* dev,
                   cudaStream_t stream, Tensor** out);
 void tensor_destroy(Tensor* t);
+// kErrInvalid unless the calling thread's current CUDA device is the tensor's
+int check_current_device(const Tensor& t);
 int tensor_sqnorm(Tensor* t, cudaStream_t stream, double* out);
 ModePlan make_plan(const Tensor& t, int mode);
 int plan_splits(const ModePlan& view);  // shape-only q-split count of a view

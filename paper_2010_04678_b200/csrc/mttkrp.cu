@@ -272,10 +272,28 @@ int tensor_create(int order, const int64_t* dims, const double* host, const doub
   return kOk;
 }
 
+int check_current_device(const Tensor& t) {
+  int cur = -1;
+  CALS_CUDA_TRY(cudaGetDevice(&cur));
+  CALS_CHECK(cur == t.device, kErrInvalid,
+             "the tensor was uploaded to CUDA device " + std::to_string(t.device) +
+                 " but the current device is " + std::to_string(cur));
+  return kOk;
+}
+
 void tensor_destroy(Tensor* t) {
   if (!t) return;
+  // The buffers may still be read by kernels queued on any stream (the
+  // engine's, an operator call's, the slicing stream): wait for the device
+  // before handing the memory back to the pool.  Destroying a tensor is rare
+  // (release_device / garbage collection), never on a hot path.
+  int prev = -1;
+  cudaGetDevice(&prev);
+  if (prev != t->device) cudaSetDevice(t->device);
+  cudaDeviceSynchronize();
   ozaki_release(*t);
   if (t->owned && t->data) cudaFreeAsync(t->data, 0);
+  if (prev >= 0 && prev != t->device) cudaSetDevice(prev);
   delete t;
 }
 

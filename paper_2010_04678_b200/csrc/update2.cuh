@@ -1,0 +1,74 @@
+// Split per-model update (ranks <= 32, Cholesky / pinv updates): the work of
+// als.py:74-96 + driver.py:213-235 divided by what the next fused MTTKRP
+// actually waits for.
+//
+//   prep(n)  -- OFF the critical path, on a side stream concurrently with the
+//               fused MTTKRP of mode n: Gram refresh of the factor updated
+//               last (G_{n-1} = A_{n-1}^T A_{n-1}; every Gram of a freshly
+//               admitted model at n = 0, driver.py:203-205), the Hadamard of
+//               the other modes' Gramians (ascending, driver.py:223-225), the
+//               finite check on H and the upper Cholesky of H (dpotrf), or
+//               the eigen pseudo-inverse when H admits none (als.py:86-96).
+//               H_n needs no M_n, so none of this waits for the contraction.
+//               One warp per model (it shares the SM with the contraction).
+//   solve(n) -- ON the critical path, right after the MTTKRP: one CTA per
+//               (model, 128-row chunk) solves its rows A = M H^-1 (dpotrs
+//               order) or A = M pinv(H), all-or-nothing on a non-finite M
+//               block (ValueError -> FAILED, als.py:84-85); the last mode also
+//               forms partial Gramians / inner products per chunk, and the
+//               chunk that arrives last per model finishes the fast error,
+//               the fit and the stopping rule (als.py:99-124,
+//               driver.py:241-273).  A non-finite Cholesky solution (the
+//               reference then redoes the block with the pinv, als.py:88-90)
+//               is redone by that last chunk too (cold path).
+//
+// Results are independent of the slot a model occupies and of the other
+// models (fixed per-model reduction orders), so CALS == SEQUENTIAL bitwise.
+#pragma once
+
+#include "engine_state.cuh"
+
+namespace cals {
+
+constexpr int kSolveRows = 128;  // rows (threads) per solve CTA
+constexpr int kPrepThreads = 32;  // one warp per model
+
+// prep / solve status of a model for the current mode
+enum PrepFlag : int { kPrepChol = 0, kPrepPinv = 1, kPrepBadH = 2, kPrepFailed = 3 };
+
+struct UpdArgs {
+  EngState* st;            // decide_model (last mode), scalars
+  const int* n_active;     // &st->n_active (device)
+  const int4* slot_info;   // {model, rank, column offset, Gramian offset}
+  int* failed;
+  int* fresh;
+  int* pflag;              // per model, PrepFlag for the current mode
+  int* arrive;             // per model arrival counter of the solve chunks
+  int* solbad;             // per model: a Cholesky solution entry was non-finite
+  double* grams;           // [order][gram_stride]
+  long long gram_stride;
+  double* ubuf;            // per model R x R: U strictly upper, 1/U[a][a] on the
+                           // diagonal (kPrepChol) or pinv(H) (kPrepPinv)
+  double* gpart;           // last mode: per model [chunk][R][R] partial Gramians
+  double* ipart;           // last mode: per model [chunk] partial <A, M>
+  const double* Mout;
+  double* F[kMaxOrder];
+  long long dims[kMaxOrder];
+  long long ld;
+  int order;
+};
+
+// Shared memory of upd_solve_kernel<RB>: U (RB^2) + 1/diag (RB) + row tile
+// (kSolveRows x pitch) + reduction scratch.
+__host__ __device__ constexpr size_t solve_smem_bytes(int RB) {
+  return size_t(RB * RB + RB + kSolveRows * (RB + 1) + 32 + RB) * 8 + 16;
+}
+
+using PrepKernel = void (*)(UpdArgs, int);
+using SolveKernel = void (*)(UpdArgs, int, int);
+// kernels of rank bucket rb (8 / 16 / 24 / 32) and the solve kernels' dynamic
+// shared memory
+void split_kernels_for(int rb, PrepKernel* prep, SolveKernel* solve, SolveKernel* last,
+                       size_t* smem);
+
+}  // namespace cals

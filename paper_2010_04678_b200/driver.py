@@ -82,11 +82,20 @@ def run(t: DenseTensor, models: Iterable[Model], cfg: ConvergenceConfig, *,
     if mode is ExecutionMode.CALS:
         return _run_fused(t, queue, cfg, r_star, trace, label_per_model=False, ls=ls,
                           nonneg=nonneg)
+    # SEQUENTIAL / PARALLEL: one instance at a time (driver.py:133-160); a
+    # numerical failure retires it with the reference's _fit_or_fail record
     out = []
     for m in queue:
         out += _run_fused(t, [m], cfg, m.rank, trace, label_per_model=True, ls=ls,
                           nonneg=nonneg)
     return out
+
+
+def _failure_record(src: Model) -> Model:
+    """_fit_or_fail's result for an instance whose update raised
+    (driver.py:148-160): the starting factors, no iterations, error nan."""
+    return Model(id=src.id, rank=src.rank, factors=src.copy_factors(), error=float("nan"),
+                 fit=-np.inf, status=ModelStatus.FAILED, meta=dict(src.meta))
 
 
 def _instance_flops(t: DenseTensor, rank: int, iterations: int) -> int:
@@ -105,7 +114,9 @@ class _EngineCache:
         self.lock = threading.Lock()
 
     def acquire(self, dev, r_star: int, ranks, trace_capacity: int) -> CalsEngine:
-        key = (tuple(dev.dims), int(r_star), tuple(int(r) for r in ranks), int(trace_capacity),
+        import torch
+
+        key = (torch.cuda.current_device(), tuple(dev.dims), int(r_star), tuple(int(r) for r in ranks), int(trace_capacity),
                os.environ.get("CALS_TREE"), os.environ.get("CALS_SPLITS"))
         with self.lock:
             for i, (k, e) in enumerate(self.free):
@@ -141,7 +152,12 @@ def clear_engine_cache() -> None:
 
 def _run_fused(t: DenseTensor, queue: list[Model], cfg: ConvergenceConfig, r_star: int,
                trace: list | None, label_per_model: bool,
-               ls: LineSearchConfig | None = None, nonneg: bool = False) -> list[Model]:
+               ls: LineSearchConfig | None = None, nonneg: bool = False,
+               raise_on_update_failure: bool = False) -> list[Model]:
+    """``label_per_model``: the run is one SEQUENTIAL / PARALLEL instance --
+    the input's status is left alone and an update failure returns the
+    reference's failure record; ``raise_on_update_failure`` (run_single_als)
+    raises ValueError instead, as update_factor does (als.py:84-85)."""
     import torch
 
     prof = LAST_RUN_PROFILE
@@ -174,6 +190,7 @@ def _run_fused(t: DenseTensor, queue: list[Model], cfg: ConvergenceConfig, r_sta
         # (they are views into it); the stream is synchronised before return
         eng.pool_download(pool_t.numpy())
         warned = eng.nnls_warnings() if nonneg else None
+        upd_failed = eng.update_failures() if label_per_model else None
         wall = time.perf_counter() - tic
         records = eng.trace() if (trace is not None and not label_per_model) else None
     except _BadNorm:
@@ -188,8 +205,9 @@ def _run_fused(t: DenseTensor, queue: list[Model], cfg: ConvergenceConfig, r_sta
     t5 = time.perf_counter()
     prof.update(tensor_upload_s=t1 - t0, engine_create_s=t2 - t1, pool_upload_s=t3 - t2,
                 upload_wait_s=tic - t3, device_loop_s=t4 - tic, results_download_s=t5 - t4)
-    for m in queue:
-        m.status = ModelStatus.ACTIVE
+    if not label_per_model:
+        for m in queue:
+            m.status = ModelStatus.ACTIVE  # admitted (driver.py:202)
     pool = pool_t.numpy()
     order = np.argsort(res.retire_seq, kind="stable").tolist()
     lam_off = np.concatenate([[0], np.cumsum(ranks)]).tolist()
@@ -200,6 +218,14 @@ def _run_fused(t: DenseTensor, queue: list[Model], cfg: ConvergenceConfig, r_sta
     try:
         for k in order:
             src = queue[k]
+            if upd_failed is not None and upd_failed[k]:
+                if raise_on_update_failure:
+                    raise ValueError("non-finite values in the factor update of model "
+                                     f"{src.id!r}")
+                rec = _failure_record(src)
+                rec.seconds_active = secs[k]
+                out.append(rec)
+                continue
             meta = dict(src.meta)
             meta["lambdas"] = lam[lam_off[k]:lam_off[k + 1]]
             out.append(Model._from_engine(id=src.id, rank=src.rank, factors=eng.unpack(pool, k),

@@ -187,6 +187,13 @@ class CalsEngine:
         _native.call("cals_engine_nnls_warnings", self.handle, flags.ctypes.data)
         return flags[:len(self.ranks)]
 
+    def update_failures(self) -> np.ndarray:
+        """Per model: a factor update saw non-finite input (the reference's
+        ValueError, als.py:84-85)."""
+        flags = np.zeros(max(len(self.ranks), 1), np.int32)
+        _native.call("cals_engine_update_failures", self.handle, flags.ctypes.data)
+        return flags[:len(self.ranks)].astype(bool)
+
     # ------------------------------------------------------- step-wise
     def begin(self, tol: float, max_iterations: int, sqnorm: float, stream=None):
         import torch

@@ -227,3 +227,44 @@ def test_dimension_tree_variants_match_reference(cals, tree, monkeypatch):
     t = cals.generate_synthetic((12, 10, 8), 3, 0.1, seed=0)
     _run_and_compare(cals, "small_refill", t, cals.build_models(t.dims, [1, 2, 3, 4], 2, seed=1),
                      1e-6, 200, 6, fac_tol=1e-6)
+
+
+@pytest.mark.parametrize("mode", ["sequential", "parallel"])
+def test_sequential_failure_record(cals, mode):
+    """SEQUENTIAL / PARALLEL follow _fit_or_fail (driver.py:148-160)
+    -- the failed instance returns its starting factors, 0 iterations, error
+    nan -- and neither input's status is touched (golden: real reference)."""
+    f = np.load(os.path.join(GOLDEN, "fail_inputs.npz"))
+    g = np.load(os.path.join(GOLDEN, "run_fail_seq.npz"))
+    t = cals.DenseTensor((4, 4, 3), f["data"])
+    good = cals.Model(id="good", rank=2, factors=[f[f"good_f{n}"] for n in range(3)])
+    bad = cals.Model(id="bad", rank=2, factors=[f[f"good_f{n}"] for n in range(3)])
+    for n in range(3):
+        bad.factors[n][...] = f[f"bad_f{n}"]
+    out = cals.run(t, [bad, good], cals.ConvergenceConfig(tol=0.0, max_iterations=3),
+                   mode=cals.ExecutionMode(mode))
+    assert [m.id for m in out] == g[f"{mode}_order"].tolist()
+    assert [m.status.value for m in out] == g[f"{mode}_status"].tolist()
+    assert [m.iterations_done for m in out] == g[f"{mode}_iterations"].tolist()
+    assert [bad.status.value, good.status.value] == g[f"{mode}_input_status"].tolist()
+    for m, e in zip(out, g[f"{mode}_error"]):
+        assert (np.isnan(m.error) and np.isnan(e)) or abs(m.error - e) <= 1e-9 * abs(e)
+        for n in range(3):
+            ref = g[f"{mode}_{m.id}_f{n}"]
+            if m.id == "bad":  # the starting factors, NaN included
+                np.testing.assert_array_equal(m.factors[n], ref)
+            else:
+                assert rel(m.factors[n], ref) <= 1e-9
+
+
+def test_single_als_raises_on_update_failure(cals):
+    f = np.load(os.path.join(GOLDEN, "fail_inputs.npz"))
+    g = np.load(os.path.join(GOLDEN, "run_fail_seq.npz"))
+    t = cals.DenseTensor((4, 4, 3), f["data"])
+    bad = cals.Model(id="bad", rank=2, factors=[f[f"good_f{n}"] for n in range(3)])
+    for n in range(3):
+        bad.factors[n][...] = f[f"bad_f{n}"]
+    assert str(g["single_raises"]) == "ValueError"
+    with pytest.raises(ValueError):
+        cals.run_single_als(t, bad, cals.ConvergenceConfig(tol=0.0, max_iterations=3))
+    assert bad.status.value == str(g["single_input_status"])
