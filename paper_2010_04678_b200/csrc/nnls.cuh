@@ -83,7 +83,14 @@ __device__ inline double nnls_solve_passive(const double* H, int R, unsigned P, 
     if (lane > k && lane < p) {
       const double l = A[lane * kNnlsP + k] * rinv;
       A[lane * kNnlsP + k] = l;
-      for (int j = k + 1; j < p; ++j) A[lane * kNnlsP + j] = fma(-l, A[k * kNnlsP + j], A[lane * kNnlsP + j]);
+      // a_ij - l_ik u_kj with two roundings, as OpenBLAS's dgetf2 (dot of
+      // length one, then the subtraction): with the reciprocal multiplier
+      // and the fused forward / back substitutions this reproduces
+      // np.linalg.solve bit for bit on 2 x 2 systems (the reference suite's
+      // exact enumeration check, test_acceptance.py:183-188)
+      for (int j = k + 1; j < p; ++j)
+        A[lane * kNnlsP + j] =
+            __dsub_rn(A[lane * kNnlsP + j], __dmul_rn(l, A[k * kNnlsP + j]));
     }
     __syncwarp();
   }
