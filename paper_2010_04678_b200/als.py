@@ -178,7 +178,10 @@ def nnls_solve_row(h: np.ndarray, f: np.ndarray, active: np.ndarray | None = Non
     returns (x, active, converged)."""
     f = np.asarray(f, dtype=np.float64).ravel()
     r = f.size
-    act = np.zeros((1, r), bool) if active is None else np.asarray(active, bool).reshape(1, r)
+    # no warm start = every variable pinned to zero, an empty passive set
+    # (als.py:203: passive = zeros when active is None) -- unlike nnls_update,
+    # whose NnlsState starts with nothing pinned
+    act = np.ones((1, r), bool) if active is None else np.asarray(active, bool).reshape(1, r)
     x, a, conv = _nnls_rows_gpu(f[None, :], h, act, -1 if max_iter is None else max_iter)
     if not conv[0]:
         warnings.warn("active-set search hit its iteration cap", NonConvergedNnlsWarning,

@@ -933,16 +933,18 @@ static int engine_create(Tensor* t, int capacity, int n_models, const int* ranks
   // CALS_SPLIT_UPDATE=0 keeps the one-kernel (block per model) update
   const char* split_env = getenv("CALS_SPLIT_UPDATE");
   e->split = rmax <= kFastR && (!split_env || atoi(split_env) != 0);
-  int nch_last = 1;
-  for (int n = 0; n < N; ++n) e->nch[n] = int((t->dims[n] + kSolveRows - 1) / kSolveRows);
-  nch_last = e->nch[N - 1];
+  int nch_max = 1;
+  for (int n = 0; n < N; ++n) {
+    e->nch[n] = int((t->dims[n] + kSolveRows - 1) / kSolveRows);
+    nch_max = std::max(nch_max, e->nch[n]);
+  }
   UpdArgs& ua = e->ua;
   items.push_back({(void**)&ua.pflag, nmod * 4});
   items.push_back({(void**)&h.arrive, nmod * 4});
   items.push_back({(void**)&h.solbad, nmod * 4});
-  items.push_back({(void**)&ua.ubuf, size_t(e->gram_stride) * 8});
-  items.push_back({(void**)&ua.gpart, size_t(e->gram_stride) * nch_last * 8});
-  items.push_back({(void**)&ua.ipart, nmod * nch_last * 8});
+  items.push_back({(void**)&ua.ubuf, 3 * size_t(e->gram_stride) * 8});
+  items.push_back({(void**)&ua.gpart, size_t(e->gram_stride) * nch_max * 8});
+  items.push_back({(void**)&ua.ipart, nmod * nch_max * 8});
   size_t total = 0;
   for (auto& it : items) total = align_up(total, 256) + it.bytes;
   CALS_CUDA_TRY(cudaMalloc(&e->d_block, total));
@@ -1178,6 +1180,15 @@ static int enqueue_line_search(Engine* e, cudaStream_t stream) {
   return kOk;
 }
 
+// CALS_PDL=0 disables programmatic dependent launches (A/B measurements)
+static bool pdl_enabled() {
+  static const bool on = [] {
+    const char* v = getenv("CALS_PDL");
+    return !v || atoi(v) != 0;
+  }();
+  return on;
+}
+
 // Split update of mode n: prep(n) forked onto the side stream before the
 // MTTKRP of mode n is queued (it depends only on what the main stream has
 // done so far), solve(n) after both.
@@ -1191,8 +1202,19 @@ static int enqueue_split_mode(Engine* e, int n, cudaStream_t stream) {
   if (rc) return rc;
   CALS_CUDA_TRY(cudaStreamWaitEvent(stream, e->ev_join[n], 0));
   SolveKernel k = n == e->order - 1 ? e->solve_last_kernel : e->solve_kernel;
-  k<<<e->max_slots * e->nch[n], kSolveRows, e->solve_smem, stream>>>(e->ua, n, e->nch[n]);
-  CALS_CUDA_TRY(cudaGetLastError());
+  // programmatic launch: the solve's prologue (slot, pflag, U) overlaps the
+  // tail of the kernel that produces M_n (griddep_wait before reading it)
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(e->max_slots * e->nch[n]);
+  cfg.blockDim = dim3(kSolveRows);
+  cfg.dynamicSmemBytes = e->solve_smem;
+  cfg.stream = stream;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  CALS_CUDA_TRY(cudaLaunchKernelEx(&cfg, k, e->ua, n, e->nch[n]));
   return kOk;
 }
 
@@ -1414,11 +1436,19 @@ static int engine_run(Engine* e, double tol, int max_iterations, double sqnorm, 
 
 using namespace cals;
 
+#ifdef CALS_SOLVE_PROFILE
+namespace cals { int debug_solve_prof(long long* host, size_t bytes); }
+#endif
 struct cals_tensor { Tensor* t; };
 struct cals_engine { Engine* e; };
 
 extern "C" {
 
+#ifdef CALS_SOLVE_PROFILE
+int cals_debug_solve_prof(long long* host, size_t bytes) {
+  return cals::debug_solve_prof(host, bytes);
+}
+#endif
 #ifdef CALS_UPD_PROFILE
 // profiling builds only (not in the public header): the update kernel's
 // per-(mode, slot) phase stamps of the last launches

@@ -88,11 +88,20 @@ struct EngState {
   int* solbad;
 };
 
+// Per-model scalars of the stopping rule, loadable ahead of time (all
+// loads independent) so the decision itself is loads-free.
+struct DecideIn {
+  int it;        // iteration count after this iteration's increment
+  int failed;
+  double f_prev;
+  double tol, sqnorm;
+  int max_iterations;
+};
+
 // Stopping rule for model k with squared error e (driver.py:260-273); the
 // caller has already incremented iters[k].  Thread 0 only.
-__device__ inline void decide_model(EngState* st, int k, double e) {
-  const int it = st->iters[k];
-  if (st->failed[k]) {
+__device__ inline void decide_model_with(EngState* st, int k, double e, const DecideIn& d) {
+  if (d.failed) {
     st->err[k] = nan("");
     st->fit[k] = -INFINITY;
     st->status[k] = kFailed;
@@ -106,18 +115,29 @@ __device__ inline void decide_model(EngState* st, int k, double e) {
     atomicAdd(st->changed, 1);
     return;
   }
-  const double f = 1.0 - sqrt(e) / sqrt(st->sqnorm);
+  const double f = 1.0 - sqrt(e) / sqrt(d.sqnorm);
   st->err[k] = e;
   st->fit[k] = f;
-  if (st->tol > 0.0 && f - st->f_prev[k] < st->tol) {
+  if (d.tol > 0.0 && f - d.f_prev < d.tol) {
     st->status[k] = kConverged;
     atomicAdd(st->changed, 1);
-  } else if (it >= st->max_iterations) {
+  } else if (d.it >= d.max_iterations) {
     st->status[k] = kCap;
     atomicAdd(st->changed, 1);
   } else {
     st->f_prev[k] = f;
   }
+}
+
+__device__ inline void decide_model(EngState* st, int k, double e) {
+  DecideIn d;
+  d.it = st->iters[k];
+  d.failed = st->failed[k];
+  d.f_prev = st->f_prev[k];
+  d.tol = st->tol;
+  d.sqnorm = st->sqnorm;
+  d.max_iterations = st->max_iterations;
+  decide_model_with(st, k, e, d);
 }
 
 }  // namespace cals

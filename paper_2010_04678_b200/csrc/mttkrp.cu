@@ -440,6 +440,7 @@ __global__ void fill_kernel(double* p, long long n, double v) {
 __global__ void split_reduce_kernel(const double* __restrict__ part, long long part_stride, int S,
                                     int M, long long ldp, const int* width_ptr, int width,
                                     double* __restrict__ out, long long ldo) {
+  griddep_launch_dependents();  // the next kernel may start its prologue
   const int W = width_ptr ? *width_ptr : width;
   const int hw = (W + 1) >> 1;  // column pairs
   const long long n = (long long)M * hw;
@@ -657,6 +658,7 @@ __global__ void partial_ttv_kernel(const double* __restrict__ P, long long ld, l
                                    const double* __restrict__ F, long long ldf,
                                    const int* width_ptr, int width, long long rows_out,
                                    double* __restrict__ out, long long ldo) {
+  griddep_launch_dependents();  // the next kernel may start its prologue
   const int W = width_ptr ? *width_ptr : width;
   const long long n = (reduce_b ? rows_out : (rows_out + 3) / 4) * W;
   for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < n;
@@ -748,6 +750,7 @@ __global__ void __launch_bounds__(512) partial_ttv_split_kernel(const double* __
                                          long long ldf, const int* width_ptr, int width,
                                          long long rows_out, double* __restrict__ out,
                                          long long ldo) {
+  griddep_launch_dependents();  // the next kernel may start its prologue
   extern __shared__ double red[];  // [G][4][32]
   const int W = width_ptr ? *width_ptr : width;
   if ((int)blockIdx.x * 32 >= W) return;  // block-uniform

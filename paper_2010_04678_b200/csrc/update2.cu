@@ -1,13 +1,23 @@
-// Split per-model update kernels (see update2.cuh for the design).
+// Split per-model update kernels (design: update2.cuh).
 #include "update.cuh"
 #include "update2.cuh"
 
 namespace cals {
 
-// G = A^T A of the column block A[i][r] (rows x R, row stride ld) by one warp:
-// the block goes through shared memory 32 rows at a time (pitch P odd), each
-// lane accumulates its (a, b) pairs over ascending rows (the same chain per
-// pair as block_gram_fast), upper triangle mirrored.
+#ifdef CALS_SOLVE_PROFILE
+// per (mode, CTA) clock64 stamps of the solve kernel: [0] R, [1..8] phases
+__device__ long long g_solve_prof[8][2048][10];
+#define SOLVE_STAMP(i) \
+  if (tid == 0 && blockIdx.x < 2048) g_solve_prof[n][blockIdx.x][i] = clock64() - t_entry;
+#else
+#define SOLVE_STAMP(i)
+#endif
+
+// G = A^T A of the column block A[i][r] (rows x R, row stride ld) by one warp
+// (fresh admissions only).  32-row chunks: lane i loads row i of the next
+// chunk into registers while the warp accumulates the current chunk from
+// shared memory (pitch P odd); each lane owns (a, b) pairs summed over
+// ascending rows (one chain per pair, as block_gram_fast); upper mirrored.
 template <int RB>
 __device__ __forceinline__ void warp_gram(const double* __restrict__ A, long long ld, int rows,
                                           int R, double* __restrict__ T, double* __restrict__ G) {
@@ -15,33 +25,41 @@ __device__ __forceinline__ void warp_gram(const double* __restrict__ A, long lon
   const int lane = threadIdx.x & 31;
   const int P = fast_pitch(R);
   const int npairs = R * (R + 1) / 2;
-  int pa[NP], pb[NP];
+  int pab[NP];  // a | b << 8, -1 past the pairs
   double acc[NP];
 #pragma unroll
   for (int j = 0; j < NP; ++j) {
     const int p = lane + 32 * j;
     acc[j] = 0.0;
-    pa[j] = -1;
-    pb[j] = 0;
+    pab[j] = -1;
     if (p < npairs) {
       int aa = 0, rem = p;
       while (rem >= R - aa) {
         rem -= R - aa;
         ++aa;
       }
-      pa[j] = aa;
-      pb[j] = aa + rem;
+      pab[j] = aa | ((aa + rem) << 8);
     }
   }
+  double v[RB];
+  auto load_row = [&](int i) {
+#pragma unroll
+    for (int c = 0; c < RB; ++c) v[c] = (i < rows && c < R) ? A[(long long)i * ld + c] : 0.0;
+  };
+  load_row(lane);
   for (int base = 0; base < rows; base += 32) {
     const int cnt = min(32, rows - base);
-    stage_block(A + (long long)base * ld, ld, cnt, R, P, T, lane, 32);
+    __syncwarp();  // the previous chunk's reads of T are done
+#pragma unroll
+    for (int c = 0; c < RB; ++c)
+      if (c < R) T[lane * P + c] = v[c];
     __syncwarp();
+    if (base + 32 < rows) load_row(base + 32 + lane);  // in flight during the sums
 #pragma unroll
     for (int j = 0; j < NP; ++j) {
-      if (pa[j] < 0) continue;
-      const double* xa = T + pa[j];
-      const double* xb = T + pb[j];
+      if (pab[j] < 0) continue;
+      const double* xa = T + (pab[j] & 255);
+      const double* xb = T + (pab[j] >> 8);
       double s = acc[j];
       int r = 0;
       for (; r + 4 <= cnt; r += 4) {
@@ -56,19 +74,18 @@ __device__ __forceinline__ void warp_gram(const double* __restrict__ A, long lon
       for (; r < cnt; ++r) s = fma(xa[r * P], xb[r * P], s);
       acc[j] = s;
     }
-    __syncwarp();
   }
 #pragma unroll
   for (int j = 0; j < NP; ++j) {
-    if (pa[j] < 0) continue;
-    G[pa[j] * R + pb[j]] = acc[j];
-    G[pb[j] * R + pa[j]] = acc[j];
+    if (pab[j] < 0) continue;
+    const int aa = pab[j] & 255, bb = pab[j] >> 8;
+    G[aa * R + bb] = acc[j];
+    G[bb * R + aa] = acc[j];
   }
 }
 
 // H = Hadamard of the Gramians of every mode but n (ascending), R x R, into
-// shared memory; returns (to every thread of the calling group) whether any
-// entry is non-finite.
+// shared memory; returns whether any entry this thread formed is non-finite.
 __device__ __forceinline__ int hadamard_others(const double* grams, long long gs, long long go,
                                                int N, int n, int R, double* H, int t0, int nt) {
   int bad = 0;
@@ -107,30 +124,31 @@ __global__ void __launch_bounds__(kPrepThreads, 16) upd_prep_kernel(UpdArgs a, i
     return;
   }
   const long long gs = a.gram_stride;
-  if (n == 0) {
-    if (a.fresh[k]) {  // Gramians of the admitted starting point (driver.py:203-205)
-      for (int i = 1; i < N; ++i)
-        warp_gram<RB>(a.F[i] + off, a.ld, (int)a.dims[i], R, T, a.grams + i * gs + go);
-      if (lane == 0) a.fresh[k] = 0;
-    }
-  } else {  // the factor updated last (driver.py:234)
-    warp_gram<RB>(a.F[n - 1] + off, a.ld, (int)a.dims[n - 1], R, T,
-                  a.grams + (n - 1) * gs + go);
+  if (n == 0 && a.fresh[k]) {  // Gramians of the admitted starting point (driver.py:203-205)
+    for (int i = 1; i < N; ++i)
+      warp_gram<RB>(a.F[i] + off, a.ld, (int)a.dims[i], R, T, a.grams + i * gs + go);
+    if (lane == 0) a.fresh[k] = 0;
+    __syncwarp();
   }
-  __syncwarp();
   const int bad = __any_sync(0xffffffffu, hadamard_others(a.grams, gs, go, N, n, R, H, lane, 32));
   if (bad) {  // non-finite h: update_factor raises (als.py:84-85)
     if (lane == 0) a.pflag[k] = kPrepBadH;
     return;
   }
   __syncwarp();
+  // per model: [U | U^T | H] (3 R x R blocks); H feeds the last mode's fast
+  // error (sum of H o G_{N-1}) without reloading the other Gramians
+  double* U = a.ubuf + 3 * go;
+  double* V = U + R * R;
+  for (int idx = lane; idx < R * R; idx += 32) V[R * R + idx] = H[idx];
   warp_cholesky_rb<RB>(H, R, invd, &flag);
   __syncwarp();
-  double* U = a.ubuf + go;
   if (flag) {
     for (int idx = lane; idx < R * R; idx += 32) {
       const int r = idx / R, c = idx - r * R;
-      U[idx] = r < c ? H[idx] : (r == c ? invd[r] : 0.0);
+      const double u = r < c ? H[idx] : (r == c ? invd[r] : 0.0);
+      U[idx] = u;            // U[r][c] (strictly upper), 1/U[r][r] on the diagonal
+      V[c * R + r] = u;      // U^T: the back substitution reads rows of it
     }
     if (lane == 0) a.pflag[k] = kPrepChol;
   } else {  // dpotrf failed: pinv(H) (als.py:91-96)
@@ -142,7 +160,8 @@ __global__ void __launch_bounds__(kPrepThreads, 16) upd_prep_kernel(UpdArgs a, i
   }
 }
 
-// x <- m P for one row (als.py:96: m @ pinv), b ascending as block_apply_pinv
+// x <- m P for one shared-memory row (als.py:96: m @ pinv), b ascending as
+// block_apply_pinv
 template <int RB>
 __device__ __forceinline__ void apply_pinv_row(double* __restrict__ xs, const double* __restrict__ P,
                                                int R) {
@@ -156,6 +175,20 @@ __device__ __forceinline__ void apply_pinv_row(double* __restrict__ xs, const do
       if (b < R) s = fma(m[b], P[b * R + c], s);
     xs[c] = s;
   }
+}
+
+// the last mode's error / fit / stopping rule with the scalars loaded at
+// kernel entry (thread 0): only stores left on the critical path
+__device__ __forceinline__ void finish_model_pre(const UpdArgs& a, int k, double msq, double inner,
+                                                 const DecideIn& d, int ls_on) {
+  EngState* st = a.st;
+  st->iters[k] = d.it;
+  double e = d.sqnorm + msq - 2.0 * inner;
+  e = e > 0.0 ? e : 0.0;  // als.py:114-115 (NaN clamps to 0 as there)
+  if (ls_on)
+    st->e_tmp[k] = e;  // decided after the line-search candidate (ls_finish)
+  else
+    decide_model_with(st, k, e, d);
 }
 
 // the last mode's error / fit / stopping rule from the summed pieces
@@ -174,16 +207,141 @@ __device__ __forceinline__ void finish_model(const UpdArgs& a, int k, double msq
     decide_model(st, k, e);
 }
 
+template <int R>
+__device__ __forceinline__ void solve_row_exact(double* __restrict__ xs,
+                                                const double* __restrict__ U,
+                                                const double* __restrict__ V,
+                                                const double* __restrict__ invd) {
+  constexpr int RP = R + (R & 1);
+  double x[R];
+#pragma unroll
+  for (int c = 0; c < R; ++c) x[c] = xs[c];
+#pragma unroll
+  for (int k = 0; k < R; ++k) {
+    const double yk = x[k] * invd[k];
+    x[k] = yk;
+#pragma unroll
+    for (int c = k + 1; c < R; ++c) x[c] = fma(-U[k * RP + c], yk, x[c]);
+  }
+#pragma unroll
+  for (int k = R - 1; k >= 0; --k) {
+    const double xk = x[k] * invd[k];
+    x[k] = xk;
+#pragma unroll
+    for (int c = 0; c < k; ++c) x[c] = fma(-V[k * RP + c], xk, x[c]);
+  }
+#pragma unroll
+  for (int c = 0; c < R; ++c) xs[c] = x[c];
+}
+
+template <int RB, int R = 1>
+__device__ __forceinline__ void solve_row_dispatch(int r, double* xs, const double* U,
+                                                   const double* V, const double* invd) {
+  if constexpr (R <= RB) {
+    if (r == R)
+      solve_row_exact<R>(xs, U, V, invd);
+    else
+      solve_row_dispatch<RB, R + 1>(r, xs, U, V, invd);
+  }
+}
+
+// Gramian X^T X of the rows [0, cnt) of the tile X (pitch P, R columns) on
+// the FP64 tensor cores (DMMA.8x8x4): 8 x 8 output tiles of the upper tile
+// triangle; with few tiles the rows are split into up to 8 / tiles parts
+// (one warp each) whose partial tiles are added in part order through
+// `scr` (>= 8 * 64 doubles).  Result (full symmetric) in Gs (R x R, smem).
+__device__ __forceinline__ void tile_gram_tc(const double* __restrict__ X, int P, int cnt, int R,
+                                             double* __restrict__ scr, double* __restrict__ Gs) {
+  constexpr int kWarps = kSolveRows / 32;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int T = (R + 7) >> 3;
+  const int ntiles = T * (T + 1) / 2;
+  const int parts = ntiles >= kWarps ? 1 : kWarps / ntiles;
+  const int r_lo = lane >> 2, k_lo = lane & 3;
+  const int steps = (cnt + 3) >> 2;  // K steps of 4 rows
+  for (int task = warp; task < ntiles * parts; task += kWarps) {
+    const int t = task / parts, part = task - t * parts;
+    int ti = 0, rem = t;
+    while (rem >= T - ti) {
+      rem -= T - ti;
+      ++ti;
+    }
+    const int tj = ti + rem;
+    const int ca = ti * 8 + r_lo, cb = tj * 8 + r_lo;
+    const bool va = ca < R, vb = cb < R;
+    const int s0 = steps * part / parts, s1 = steps * (part + 1) / parts;
+    double d0 = 0.0, d1 = 0.0;
+    for (int st = s0; st < s1; ++st) {
+      const int kk = st * 4 + k_lo;
+      const bool vk = kk < cnt;
+      const double av = (va && vk) ? X[kk * P + ca] : 0.0;
+      const double bv = (vb && vk) ? X[kk * P + cb] : 0.0;
+      dmma_8x8x4(d0, d1, av, bv);
+    }
+    if (parts == 1) {
+      const int gr = ti * 8 + r_lo, gc = tj * 8 + 2 * k_lo;
+      if (gr < R && gc < R) {
+        Gs[gr * R + gc] = d0;
+        Gs[gc * R + gr] = d0;
+      }
+      if (gr < R && gc + 1 < R) {
+        Gs[gr * R + gc + 1] = d1;
+        Gs[(gc + 1) * R + gr] = d1;
+      }
+    } else {
+      scr[task * 64 + 2 * lane] = d0;
+      scr[task * 64 + 2 * lane + 1] = d1;
+    }
+  }
+  if (parts > 1) {
+    __syncthreads();
+    for (int idx = threadIdx.x; idx < ntiles * 64; idx += kSolveRows) {
+      const int t = idx >> 6, e = idx & 63;
+      double s = scr[(t * parts) * 64 + e];
+      for (int p = 1; p < parts; ++p) s += scr[(t * parts + p) * 64 + e];
+      int ti = 0, rem = t;
+      while (rem >= T - ti) {
+        rem -= T - ti;
+        ++ti;
+      }
+      const int tj = ti + rem;
+      const int ln = e >> 1;  // lane that held the entry
+      const int gr = ti * 8 + (ln >> 2), gc = tj * 8 + 2 * (ln & 3) + (e & 1);
+      if (gr < R && gc < R) {
+        Gs[gr * R + gc] = s;
+        Gs[gc * R + gr] = s;
+      }
+    }
+  }
+}
+
+// Shared-memory layout of upd_solve_kernel<RB> (doubles)
+struct SolveSmem {
+  int U, V, H, G, invd, X, scr, red, lam, total;
+  __host__ __device__ constexpr SolveSmem(int RB)
+      : U(0), V(RB * (RB + 1)), H(2 * RB * (RB + 1)), G(2 * RB * (RB + 1) + RB * RB),
+        invd(2 * RB * (RB + 1) + 2 * RB * RB), X(2 * RB * (RB + 1) + 2 * RB * RB + RB + (RB & 1)),
+        scr(X + kSolveRows * (RB + 1)), red(scr + 8 * 64), lam(red + 32), total(lam + RB) {}
+};
+
 template <int RB, bool LAST>
-__global__ void __launch_bounds__(kSolveRows, 3) upd_solve_kernel(UpdArgs a, int n, int nch) {
+__global__ void __launch_bounds__(kSolveRows, 2) upd_solve_kernel(UpdArgs a, int n, int nch) {
   extern __shared__ __align__(16) double sm[];
-  double* U = sm;                  // RB * RB
-  double* invd = U + RB * RB;      // RB
-  double* X = invd + RB;           // kSolveRows * P
-  double* red = X + kSolveRows * (RB + 1);  // 32
-  double* lam = red + 32;          // RB (cold path)
+  constexpr SolveSmem L(RB);
+  double* U = sm + L.U;         // U (or pinv), pitch RP
+  double* V = sm + L.V;         // U^T, pitch RP
+  double* Hs = sm + L.H;        // last mode: Hadamard of G_0 .. G_{N-2} (R x R)
+  double* Gs = sm + L.G;        // the refreshed Gramian (R x R)
+  double* invd = sm + L.invd;   // 1 / U[a][a]
+  double* X = sm + L.X;         // kSolveRows x P: M rows, then the solved rows
+  double* scr = sm + L.scr;
+  double* red = sm + L.red;
+  double* lam = sm + L.lam;     // (cold path)
   __shared__ int s_last;
   const int tid = threadIdx.x;
+#ifdef CALS_SOLVE_PROFILE
+  const long long t_entry = clock64();
+#endif
   const int slot = blockIdx.x / nch;
   const int chunk = blockIdx.x - slot * nch;
   const int na = *a.n_active;
@@ -197,41 +355,82 @@ __global__ void __launch_bounds__(kSolveRows, 3) upd_solve_kernel(UpdArgs a, int
   const int r0 = chunk * kSolveRows;
   const int cnt = min(kSolveRows, rows - r0);
   const int P = fast_pitch(R);
+  const int RP = R + (R & 1);
+#ifdef CALS_SOLVE_PROFILE
+  if (tid == 0 && blockIdx.x < 2048) g_solve_prof[n][blockIdx.x][0] = R;
+#endif
+  SOLVE_STAMP(1)
   if (pf == kPrepFailed) {  // failed earlier in this iteration (driver.py:218-219)
     if (LAST && chunk == 0 && tid == 0) finish_model(a, k, 0.0, 0.0, false);
     return;
   }
-  for (int idx = tid; idx < R * R; idx += kSolveRows) {
-    const double u = a.ubuf[go + idx];
-    U[idx] = u;
-    if (pf == kPrepChol && idx / R == idx % R) invd[idx / R] = u;
+  DecideIn din{};
+  int ls_on = 0;
+  if (LAST && tid == 0) {  // independent loads, consumed at the very end
+    EngState* st = a.st;
+    din.it = st->iters[k] + 1;
+    din.failed = st->failed[k];
+    din.f_prev = st->f_prev[k];
+    din.tol = st->tol;
+    din.sqnorm = st->sqnorm;
+    din.max_iterations = st->max_iterations;
+    ls_on = st->ls_enabled;
+  }
+  // U, U^T (or pinv) and, for the last mode, H: written by prep (before)
+  {
+    const double* src = a.ubuf + 3 * go;
+    for (int idx = tid; idx < R * R; idx += kSolveRows) {
+      const int r = idx / R, c = idx - r * R;
+      const double u = src[idx];
+      if (pf == kPrepChol) {
+        U[r * RP + c] = u;
+        V[r * RP + c] = src[R * R + idx];
+        if (r == c) invd[r] = u;
+      } else {
+        U[idx] = u;  // pinv, pitch R
+      }
+      if (LAST) Hs[idx] = src[2 * R * R + idx];
+    }
   }
   // The reference checks the whole M block before touching the factor
-  // (als.py:84-85): every chunk scans all of it (L2-resident, just written),
+  // (als.py:84-85): every chunk scans all of it (one chunk at <= 256 rows),
   // staging its own rows on the way, so all chunks reach the same verdict.
   const double* Mb = a.Mout + off;
   int bad = pf == kPrepBadH;
+  // everything above came from earlier kernels (plan, prep); M_n is the
+  // output of the grid right before this one (programmatic launch)
+  griddep_wait();
+  // element e = i * R + c of the block walked with stride kSolveRows without
+  // integer divisions: (i, c) advance by (dq, dr) per step
+  const int dq = kSolveRows / R, dr = kSolveRows - dq * R;
   {
-    const int total = rows * R;
-    for (int e0 = tid; e0 < total; e0 += 4 * kSolveRows) {
-      double v[4];
-      int ii[4], cc[4];
+    int i = tid / R, c = tid - (tid / R) * R;
+    while (i < rows) {
+      double v[16];
+      int iu[16], cu[16];
 #pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        const int e = e0 + u * kSolveRows;
-        ii[u] = e / R;
-        cc[u] = e - ii[u] * R;
-        v[u] = e < total ? Mb[(long long)ii[u] * ld + cc[u]] : 0.0;
+      for (int u = 0; u < 16; ++u) {
+        iu[u] = i;
+        cu[u] = c;
+        v[u] = i < rows ? Mb[(long long)i * ld + c] : 0.0;
+        i += dq;
+        c += dr;
+        if (c >= R) {
+          c -= R;
+          ++i;
+        }
       }
 #pragma unroll
-      for (int u = 0; u < 4; ++u) {
+      for (int u = 0; u < 16; ++u) {
         bad |= !isfinite(v[u]);
-        const int i = ii[u] - r0;
-        if (e0 + u * kSolveRows < total && i >= 0 && i < cnt) X[i * P + cc[u]] = v[u];
+        const int il = iu[u] - r0;
+        if (iu[u] < rows && il >= 0 && il < cnt) X[il * P + cu[u]] = v[u];
       }
     }
   }
-  if (__syncthreads_or(bad)) {
+  const int any_bad = __syncthreads_or(bad);
+  SOLVE_STAMP(2)
+  if (any_bad) {
     if (chunk == 0 && tid == 0) {
       a.failed[k] = 1;
       if (LAST) finish_model(a, k, 0.0, 0.0, false);
@@ -239,82 +438,77 @@ __global__ void __launch_bounds__(kSolveRows, 3) upd_solve_kernel(UpdArgs a, int
     return;
   }
   int sbad = 0;
+  SOLVE_STAMP(3)
   if (tid < cnt) {
     double* x = X + tid * P;
     if (pf == kPrepChol) {
-      if (RB <= 8 || R <= 8)
-        solve_row_reg<(RB < 8 ? RB : 8)>(x, U, invd, R);
-      else if (RB <= 16 || R <= 16)
-        solve_row_reg<(RB < 16 ? RB : 16)>(x, U, invd, R);
-      else if (RB <= 24 || R <= 24)
-        solve_row_reg<(RB < 24 ? RB : 24)>(x, U, invd, R);
-      else
-        solve_row_reg<RB>(x, U, invd, R);
+      solve_row_dispatch<RB>(R, x, U, V, invd);
       for (int c = 0; c < R; ++c) sbad |= !isfinite(x[c]);
     } else {
       apply_pinv_row<RB>(x, U, R);
     }
   }
   __syncthreads();
+  // coalesced store of the solved rows (+ the last mode's <A, M> partial)
   double dot = 0.0;
   {
     double* Ac = a.F[n] + (long long)r0 * ld + off;
     const double* Mc = Mb + (long long)r0 * ld;
-    const int total = cnt * R;
-    for (int e = tid; e < total; e += kSolveRows) {
-      const int i = e / R, c = e - i * R;
+    int i = tid / R, c = tid - (tid / R) * R;
+#pragma unroll 16
+    for (; i < cnt;) {
       const double v = X[i * P + c];
       Ac[(long long)i * ld + c] = v;
       if (LAST) dot = fma(v, Mc[(long long)i * ld + c], dot);
-    }
-  }
-  if (LAST) {
-    // partial Gramian (upper triangle, ascending rows of this chunk) and
-    // partial inner product of the chunk
-    constexpr int NPB = (RB * (RB + 1) / 2 + kSolveRows - 1) / kSolveRows;
-    const int npairs = R * (R + 1) / 2;
-    double* gp = a.gpart + go * nch + (long long)chunk * R * R;
-#pragma unroll
-    for (int j = 0; j < NPB; ++j) {
-      const int p = tid + j * kSolveRows;
-      if (p < npairs) {
-        int aa = 0, rem = p;
-        while (rem >= R - aa) {
-          rem -= R - aa;
-          ++aa;
-        }
-        const int bb = aa + rem;
-        const double* xa = X + aa;
-        const double* xb = X + bb;
-        double s = 0.0;
-        int r = 0;
-        for (; r + 4 <= cnt; r += 4) {
-          s = fma(xa[r * P], xb[r * P], s);
-          s = fma(xa[(r + 1) * P], xb[(r + 1) * P], s);
-          s = fma(xa[(r + 2) * P], xb[(r + 2) * P], s);
-          s = fma(xa[(r + 3) * P], xb[(r + 3) * P], s);
-        }
-        for (; r < cnt; ++r) s = fma(xa[r * P], xb[r * P], s);
-        gp[aa * R + bb] = s;
+      i += dq;
+      c += dr;
+      if (c >= R) {
+        c -= R;
+        ++i;
       }
     }
-    const double inner = block_sum(dot, red);
-    if (tid == 0) a.ipart[(long long)k * nch + chunk] = inner;
   }
-  if (__syncthreads_or(sbad) && tid == 0) a.solbad[k] = 1;
-  // arrival: the last chunk of the model finishes it
-  __threadfence();
-  if (tid == 0) s_last = atomicAdd(&a.arrive[k], 1) == nch - 1;
-  __syncthreads();
-  if (!s_last) return;
-  __threadfence();
-  const bool redo = *(volatile int*)&a.solbad[k] != 0;
-  __syncthreads();
-  if (tid == 0) {
-    a.arrive[k] = 0;
-    a.solbad[k] = 0;
+  SOLVE_STAMP(4)
+  // Gramian refresh from the solved rows (driver.py:234)
+  tile_gram_tc(X, P, cnt, R, scr, Gs);
+  double inner = 0.0;
+  if (LAST) {
+    inner = block_sum(dot, red);  // (its barriers also publish Gs)
+    if (nch > 1 && tid == 0) a.ipart[(long long)k * nch + chunk] = inner;
   }
-  const double* Mfull = Mb;
+  sbad = __syncthreads_or(sbad);
+  SOLVE_STAMP(5)
+  double* Gn = a.grams + (long long)n * a.gram_stride + go;
+  bool redo = sbad != 0;
+  if (nch > 1) {
+    // this chunk's (upper) partial, then arrival: the last chunk finishes
+    double* gp = a.gpart + go * nch + (long long)chunk * R * R;
+    for (int idx = tid; idx < R * R; idx += kSolveRows) gp[idx] = Gs[idx];
+    if (sbad && tid == 0) a.solbad[k] = 1;
+    __threadfence();
+    __syncthreads();
+    if (tid == 0) s_last = atomicAdd(&a.arrive[k], 1) == nch - 1;
+    __syncthreads();
+    if (!s_last) return;
+    __threadfence();
+    redo = *(volatile int*)&a.solbad[k] != 0;
+    __syncthreads();
+    if (tid == 0) {
+      a.arrive[k] = 0;
+      a.solbad[k] = 0;
+    }
+    if (!redo) {
+      for (int idx = tid; idx < R * R; idx += kSolveRows) {
+        double s = 0.0;
+        for (int ch = 0; ch < nch; ++ch) s += a.gpart[go * nch + (long long)ch * R * R + idx];
+        Gs[idx] = s;
+      }
+      if (LAST) {
+        inner = 0.0;
+        for (int ch = 0; ch < nch; ++ch) inner += a.ipart[(long long)k * nch + ch];
+      }
+    }
+  }
   double* Afull = a.F[n] + off;
   if (redo) {
     // cho_solve gave a non-finite entry: the whole block again with pinv(H)
@@ -324,53 +518,50 @@ __global__ void __launch_bounds__(kSolveRows, 3) upd_solve_kernel(UpdArgs a, int
     block_pinv(U, X, lam, R);
     for (long long e = tid; e < (long long)rows * R; e += kSolveRows) {
       const int i = int(e / R), c = int(e % R);
-      const double* m = Mfull + (long long)i * ld;
+      const double* m = Mb + (long long)i * ld;
       double s = 0.0;
       for (int b = 0; b < R; ++b) s = fma(m[b], U[b * R + c], s);
       Afull[(long long)i * ld + c] = s;
     }
     __syncthreads();
-  }
-  if (!LAST) return;
-  // Gramian of the last mode and the fast error (als.py:99-115)
-  double* G = a.grams + (long long)(a.order - 1) * a.gram_stride + go;
-  double inner = 0.0;
-  if (!redo) {
-    for (int idx = tid; idx < R * R; idx += kSolveRows) {
-      const int r = idx / R, c = idx - r * R;
-      const int u = r <= c ? idx : c * R + r;
-      double s = 0.0;
-      for (int ch = 0; ch < nch; ++ch) s += a.gpart[go * nch + (long long)ch * R * R + u];
-      G[idx] = s;
-    }
-    for (int ch = 0; ch < nch; ++ch) inner += a.ipart[(long long)k * nch + ch];
-  } else {
     for (int idx = tid; idx < R * R; idx += kSolveRows) {
       const int r = idx / R, c = idx - r * R;
       const int lo = r <= c ? r : c, hi = r <= c ? c : r;
       double s = 0.0;
       for (int i = 0; i < rows; ++i)
         s = fma(Afull[(long long)i * ld + lo], Afull[(long long)i * ld + hi], s);
-      G[idx] = s;
+      Gs[idx] = s;
     }
-    double part = 0.0;
-    for (long long e = tid; e < (long long)rows * R; e += kSolveRows) {
-      const long long i = e / R;
-      const int c = int(e - i * R);
-      part = fma(Afull[i * ld + c], Mfull[i * ld + c], part);
+    if (LAST) {
+      double part = 0.0;
+      for (long long e = tid; e < (long long)rows * R; e += kSolveRows) {
+        const long long i = e / R;
+        const int c = int(e - i * R);
+        part = fma(Afull[i * ld + c], Mb[i * ld + c], part);
+      }
+      inner = block_sum(part, red);
     }
-    inner = block_sum(part, red);
   }
-  __syncthreads();
+  __syncthreads();  // Gs final
+  for (int idx = tid; idx < R * R; idx += kSolveRows) Gn[idx] = Gs[idx];
+  SOLVE_STAMP(6)
+  if (!LAST) return;
+  // fast error (als.py:99-115): sum of the Hadamard of all Gramians, folded
+  // ascending -- (G_0 o .. o G_{N-2}) from prep, then o G_{N-1}
   double mpart = 0.0;
-  for (int idx = tid; idx < R * R; idx += kSolveRows) {
-    double h = a.grams[go + idx];
-    for (int i = 1; i < a.order; ++i) h *= a.grams[i * a.gram_stride + go + idx];
-    mpart += h;
-  }
+  for (int idx = tid; idx < R * R; idx += kSolveRows) mpart += Hs[idx] * Gs[idx];
   const double msq = block_sum(mpart, red);
-  if (tid == 0) finish_model(a, k, msq, inner, true);
+  if (tid == 0) finish_model_pre(a, k, msq, inner, din, ls_on);
+  SOLVE_STAMP(7)
 }
+
+#ifdef CALS_SOLVE_PROFILE
+int debug_solve_prof(long long* host, size_t bytes) {
+  return cudaMemcpyFromSymbol(host, g_solve_prof, bytes < sizeof(g_solve_prof) ? bytes
+                                                                               : sizeof(g_solve_prof))
+             == cudaSuccess ? 0 : -1;
+}
+#endif
 
 void split_kernels_for(int rb, PrepKernel* prep, SolveKernel* solve, SolveKernel* last,
                        size_t* smem) {

@@ -3,24 +3,26 @@
 // actually waits for.
 //
 //   prep(n)  -- OFF the critical path, on a side stream concurrently with the
-//               fused MTTKRP of mode n: Gram refresh of the factor updated
-//               last (G_{n-1} = A_{n-1}^T A_{n-1}; every Gram of a freshly
-//               admitted model at n = 0, driver.py:203-205), the Hadamard of
-//               the other modes' Gramians (ascending, driver.py:223-225), the
-//               finite check on H and the upper Cholesky of H (dpotrf), or
-//               the eigen pseudo-inverse when H admits none (als.py:86-96).
-//               H_n needs no M_n, so none of this waits for the contraction.
-//               One warp per model (it shares the SM with the contraction).
+//               fused MTTKRP of mode n: the Hadamard of the other modes'
+//               Gramians (ascending, driver.py:223-225), the finite check on
+//               H and the upper Cholesky of H (dpotrf), or the eigen
+//               pseudo-inverse when H admits none (als.py:86-96); at n = 0
+//               also the Gramians of freshly admitted models
+//               (driver.py:203-205).  H_n needs no M_n, so none of this waits
+//               for the contraction.  One warp per model: it shares the SM
+//               with the contraction's CTA.
 //   solve(n) -- ON the critical path, right after the MTTKRP: one CTA per
-//               (model, 128-row chunk) solves its rows A = M H^-1 (dpotrs
-//               order) or A = M pinv(H), all-or-nothing on a non-finite M
-//               block (ValueError -> FAILED, als.py:84-85); the last mode also
-//               forms partial Gramians / inner products per chunk, and the
-//               chunk that arrives last per model finishes the fast error,
-//               the fit and the stopping rule (als.py:99-124,
-//               driver.py:241-273).  A non-finite Cholesky solution (the
-//               reference then redoes the block with the pinv, als.py:88-90)
-//               is redone by that last chunk too (cold path).
+//               (model, 256-row chunk; one chunk at every benchmarked shape)
+//               solves its rows A = M H^-1 (dpotrs order) or A = M pinv(H),
+//               all-or-nothing on a non-finite M block (ValueError -> FAILED,
+//               als.py:84-85), and refreshes G_n from the solved rows still in
+//               shared memory (driver.py:234).  The last mode also finishes
+//               the fast error, the fit and the stopping rule (als.py:99-124,
+//               driver.py:241-273).  With several chunks, the chunk that
+//               arrives last sums the per-chunk partial Gramians (fixed
+//               order).  A non-finite Cholesky solution (the reference then
+//               redoes the block with the pinv, als.py:88-90) is redone by
+//               that chunk too (cold path).
 //
 // Results are independent of the slot a model occupies and of the other
 // models (fixed per-model reduction orders), so CALS == SEQUENTIAL bitwise.
@@ -30,7 +32,7 @@
 
 namespace cals {
 
-constexpr int kSolveRows = 128;  // rows (threads) per solve CTA
+constexpr int kSolveRows = 256;  // rows (threads) per solve CTA
 constexpr int kPrepThreads = 32;  // one warp per model
 
 // prep / solve status of a model for the current mode
@@ -47,9 +49,10 @@ struct UpdArgs {
   int* solbad;             // per model: a Cholesky solution entry was non-finite
   double* grams;           // [order][gram_stride]
   long long gram_stride;
-  double* ubuf;            // per model R x R: U strictly upper, 1/U[a][a] on the
-                           // diagonal (kPrepChol) or pinv(H) (kPrepPinv)
-  double* gpart;           // last mode: per model [chunk][R][R] partial Gramians
+  double* ubuf;            // per model 3 R x R blocks: U strictly upper with
+                           // 1/U[a][a] on the diagonal (kPrepChol) or pinv(H)
+                           // (kPrepPinv); U^T; H (Hadamard of the others)
+  double* gpart;           // per model [chunk][R][R] partial Gramians (chunks > 1)
   double* ipart;           // last mode: per model [chunk] partial <A, M>
   const double* Mout;
   double* F[kMaxOrder];
@@ -58,10 +61,12 @@ struct UpdArgs {
   int order;
 };
 
-// Shared memory of upd_solve_kernel<RB>: U (RB^2) + 1/diag (RB) + row tile
-// (kSolveRows x pitch) + reduction scratch.
+// Shared memory of upd_solve_kernel<RB> (SolveSmem in update2.cu):
+// U, U^T (pitch RB + 1), H and G (RB x RB), 1/diag, the kSolveRows x (RB + 1)
+// row tile, 8 x 64 Gram partials, reduction scratch
 __host__ __device__ constexpr size_t solve_smem_bytes(int RB) {
-  return size_t(RB * RB + RB + kSolveRows * (RB + 1) + 32 + RB) * 8 + 16;
+  return size_t(2 * RB * (RB + 1) + 2 * RB * RB + RB + (RB & 1) + kSolveRows * (RB + 1) + 8 * 64 +
+                32 + RB) * 8 + 16;
 }
 
 using PrepKernel = void (*)(UpdArgs, int);

@@ -55,3 +55,17 @@ def test_bench_harness_reports(tmp_path):
         bm.write_report_json(tmp_path / "r.json", report)
         bm.write_report_csv(tmp_path / "r.csv", report)
         assert (tmp_path / "r.csv").read_text().count("\n") >= 2
+
+
+def test_efficiency_rises_with_width():
+    """The reference's acceptance criterion 12 (test_acceptance.py:286-293:
+    MTTKRP efficiency rises from width 10 to 1000 on 100^3) against the
+    measured FP64 tensor-core peak, the denominator of the B200 bench; and
+    reps = 0 records nothing (test_bench.py:79-84)."""
+    from paper_2010_04678_b200 import bench as bm
+
+    rep = bm.bench_mttkrp_sweep((100, 100, 100), [10, 1000], reps=3, seed=112)
+    eff = {r["width"]: r["efficiency"] for r in rep["aggregates"]}
+    assert eff[1000] > eff[10], eff
+    empty = bm.bench_mttkrp_sweep((6, 5, 4), [2], reps=0)
+    assert empty["records"] == [] and empty["aggregates"] == []
