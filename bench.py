@@ -72,6 +72,14 @@ WORKLOADS = {
                tol=0.0, iters=5, r_star=None, shard=True,
                desc="c4: 500x500x500 dense FP64, 500 models (ranks 1..20 x 25) split by "
                     "rank-balanced model batches over the GPUs, 5 iterations"),
+    # config 5: the tensor itself is sharded on mode 0 (rows split over the
+    # ranks, each rank generates only its slab); all-reduce of the partial
+    # MTTKRPs of modes 1, 2 and the mode-0 Gramians every iteration
+    "c5": dict(dims=(2000, 2000, 1000), true_rank=20, ranks=list(range(1, 21)), per_rank=5,
+               tol=0.0, iters=5, r_star=1050, shard=False, mode0=True,
+               desc="c5: 2000x2000x1000 dense FP64 (32 GB) sharded on mode 0 over the GPUs "
+                    "(per-rank slab generated on the device), 100 models (ranks 1..20 x 5), "
+                    "5 iterations, all-reduce of the partial MTTKRPs"),
 }
 
 
@@ -101,6 +109,16 @@ def _config(name: str, world: int) -> dict:
                          f"model-batch x{world} (every rank its own batch), tensor replicated, "
                          f"no collective"),
          "l2": "flushed between steps (256 MiB write)"}
+    if wl.get("mode0"):
+        from paper_2010_04678_b200.parallel import row_ranges
+
+        c["models_total"] = len(ranks)
+        c["models_per_gpu"] = len(ranks)
+        c["parallelism"] = (f"mode-0 tensor sharding x{world} (rows {row_ranges(wl['dims'][0], world)}),"
+                            f" every rank runs all models on its slab; NCCL all-reduce of the "
+                            f"partial MTTKRPs of modes 1, 2 and the mode-0 Gramians per iteration")
+        c["data_note"] = ("generate_synthetic's signal factors, noise drawn per 50-row block on "
+                          "the device (parallel.synthetic_slab)")
     if wl["shard"]:
         c["widths_per_rank"] = shard_widths(ranks, world)
         c["models_per_rank"] = [len(s) for s in __import__(
@@ -279,6 +297,12 @@ def run_reference_arm(args) -> None:
         return
     name = args.config or ("c2" if args.gpus <= 1 else "c4")
     threads = os.cpu_count() or 1
+    if WORKLOADS[name].get("mode0"):
+        print(json.dumps({"impl": "reference", "unavailable":
+                          "c5 needs the 32 GB tensor plus a 33.6 GB Khatri-Rao workspace in host "
+                          "memory (SURVEY.md 8(d)); the reference has no sharded path"}),
+              flush=True)
+        return
     w = _CpuWorkload(name, world)
     w.run(threads, iters=1)
     for _ in range(args.warmup):
@@ -326,6 +350,8 @@ def main_gpu(args) -> None:
     name = args.config or ("c2" if world <= 1 else "c4")
     wl = WORKLOADS[name]
     dims = wl["dims"]
+    if wl.get("mode0"):
+        return main_mode0(args, name, rank, world, local)
     t = cals.generate_synthetic(dims, wl["true_rank"], 0.1, seed=0)
     if wl["shard"]:  # fixed total work split over the ranks (strong scaling)
         from paper_2010_04678_b200.parallel import snake_partition
@@ -514,6 +540,98 @@ def main_gpu(args) -> None:
     if rank == 0:
         print(json.dumps(line), flush=True)
     eng.close()
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def main_mode0(args, name: str, rank: int, world: int, local: int) -> None:
+    """Config 5: the tensor sharded on mode 0.  Each rank
+    generates its row slab on its GPU, runs every model on it and all-reduces
+    the partial MTTKRPs (modes >= 1) and the mode-0 Gramians per driver
+    iteration (parallel.drive_mode0_sharded).  `value`: models / s of the
+    whole sweep (max over ranks of the device time, CUDA events)."""
+    import torch
+    import torch.distributed as dist
+
+    import paper_2010_04678_b200 as cals
+    from paper_2010_04678_b200.parallel import Mode0Shard, row_ranges, synthetic_slab
+
+    wl = WORKLOADS[name]
+    dims = wl["dims"]
+    if os.environ.get("CALS_C5_DIMS"):  # down-scaled smoke runs of the c5 harness
+        dims = tuple(int(x) for x in os.environ["CALS_C5_DIMS"].split(","))
+    stream = torch.cuda.current_stream()
+    rows = row_ranges(dims[0], world)[rank]
+    tic = time.perf_counter()
+    slab, sq = synthetic_slab(dims, rows, wl["true_rank"], 0.1, seed=0, block_rows=50)
+    torch.cuda.synchronize()
+    t_gen = time.perf_counter() - tic
+    models = cals.build_models(dims, wl["ranks"], wl["per_rank"], seed=1)
+    W = sum(m.rank for m in models)
+    shard = Mode0Shard(slab, rows, dims, models, r_star=W)
+    iters_run = []
+
+    def step():
+        iters_run.append(shard.sweep(wl["tol"], wl["iters"], sq))
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    clocks = ClockSampler(local).start()
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+          for _ in range(args.steps)]
+    for i in range(args.steps):
+        ev[i][0].record(stream)
+        step()
+        ev[i][1].record(stream)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    ms = sum(a.elapsed_time(b) for a, b in ev) / args.steps
+    clk = clocks.stop()
+    tmax = torch.tensor([ms], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(tmax, op=dist.ReduceOp.MAX)
+    ms_max = float(tmax.item())
+    # e2e: the pool's H2D (starting factors from host memory), the sweep,
+    # and the results D2H + gather of the A0 row blocks, wall clock
+    host_pool = shard.pool.cpu().pin_memory()
+    e2e_times = []
+    for _ in range(max(2, min(args.steps, 3))):
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        tic = time.perf_counter()
+        shard.pool.copy_(host_pool, non_blocking=True)
+        shard.sweep(wl["tol"], wl["iters"], sq)
+        out = shard.results()
+        torch.cuda.synchronize()
+        e2e_times.append(time.perf_counter() - tic)
+        assert len(out) == len(models)
+    te = torch.tensor([float(np.mean(e2e_times))], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(te, op=dist.ReduceOp.MAX)
+    flops = 3 * wl["iters"] * 2 * W * float(np.prod(dims))  # driver.py:124-125 model
+    line = {"metric": _metric(name), "value": len(models) / (ms_max * 1e-3), "unit": "models/s",
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_max,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic, generated per rank on the device (see config.data_note)",
+            "config": _config(name, world), "clocks": clk,
+            "details": {"driver_iterations_per_step": float(np.mean(iters_run)),
+                        "slab_rows": list(rows), "slab_generation_s": t_gen,
+                        "sweep_mttkrp_tflops_reference_model": flops / (ms_max * 1e-3) / 1e12,
+                        "allreduce_bytes_per_iteration": 8 * W * (dims[1] + dims[2]) +
+                        8 * sum(m.rank ** 2 for m in models)},
+            "e2e": {"value": len(models) / float(te.item()), "unit": "models/s",
+                    "h2d_bytes_per_step": int(host_pool.numel() * 8),
+                    "d2h_bytes_per_step": int(host_pool.numel() * 8),
+                    "timing": "wall clock: pool H2D + sweep + results D2H / gather, max over ranks"},
+            "gpu_launches": None, "roofline": None}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    shard.close()
     if world > 1:
         dist.destroy_process_group()
 

@@ -75,3 +75,51 @@ def test_world_size_two_gloo_gather():
     parts = snake_partition([1, 2, 3, 4, 5, 6, 7], 2)
     assert ids == [f"m{i}" for i in parts[0]] + [f"m{i}" for i in parts[1]]
     assert [it for _, it in res[0]] == [0] * len(parts[0]) + [1] * len(parts[1])
+
+
+def _slab_worker(rank, world, port, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_2010_04678_b200.parallel import row_ranges, synthetic_slab
+
+    dims = (40, 6, 5)
+    r0, r1 = row_ranges(dims[0], world)[rank]
+    slab, sq = synthetic_slab(dims, (r0, r1), 3, 0.1, seed=7, block_rows=10, device="cpu")
+    parts = [None] * world
+    dist.all_gather_object(parts, (r0, r1, slab.numpy()))
+    if rank == 0:
+        full = np.empty(dims, order="F")
+        for a, b, d in parts:
+            full[a:b] = d.reshape((b - a,) + dims[1:], order="F")
+        q.put((sq, full))
+    dist.destroy_process_group()
+
+
+def _slab(world):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_slab_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    out = q.get(timeout=120)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    return out
+
+
+def test_config5_slab_generator_gloo():
+    """The per-rank slab generator (config 5) builds one tensor whatever the
+    world size: signal from generate_synthetic's factors (io.py:114-136),
+    noise per fixed row block, norms all-reduced over gloo."""
+    sq1, t1 = _slab(1)
+    sq4, t4 = _slab(4)
+    assert np.array_equal(t1, t4)
+    assert abs(sq1 - sq4) <= 1e-12 * sq1
+    rng = np.random.default_rng(7)
+    fac = [rng.random((d, 3)) for d in (40, 6, 5)]
+    signal = np.einsum("ir,jr,kr->ijk", *fac)
+    noise = t1 - signal
+    assert abs(np.linalg.norm(noise) / np.linalg.norm(signal) - 0.1) < 1e-9
