@@ -120,5 +120,14 @@ int main() {
   run<64, 7, 2>(sms);
   run<128, 3, 2>(sms);
   run<32, 7, 2>(sms);
+  // candidates for a wider Ozaki tile (groups split over passes)
+  run<128, 4, 1>(sms);
+  run<128, 4, 2>(sms);
+  run<112, 4, 1>(sms);
+  run<112, 4, 2>(sms);
+  run<96, 5, 1>(sms);
+  run<96, 5, 2>(sms);
+  run<256, 2, 1>(sms);
+  run<256, 2, 2>(sms);
   return 0;
 }
