@@ -18,7 +18,8 @@ sweep.
             persist between calls (the driver's engine cache).
   roofline -- the fused MTTKRP (+ Lo slicing + split reduction) at the c2
             shape and W=2100 through cals_mttkrp, CUDA events.  On the INT8
-            tensor-core (Ozaki) path: executed INT8 ops against the INT8 peak
+            tensor-core (Ozaki) path: algorithmic INT8 ops (2 x 28 slice
+            products x W x prod(dims), unpadded) against the INT8 peak
             measured live by cals_int8_peak_probe, plus the FP64-equivalent
             rate (2*W*prod(dims) per launch, mttkrp.py:72-76) against the live
             DMMA peak (cals_fp64_peak_probe); on the DMMA path the latter only.
@@ -482,20 +483,28 @@ def main_gpu(args) -> None:
     fp64_eq = flops / (np.mean(per_mode) * 1e-3) / 1e12
     int8 = all(k == 1 for k in kinds)
     traffic = None
-    prof = os.path.join(ROOT, "profiles", "r01_ozaki_ncu.json" if int8 else "r01_mttkrp_ncu.json")
+    prof = os.path.join(ROOT, "profiles", "r02_ozaki_ncu.json" if int8 else "r01_mttkrp_ncu.json")
     if os.path.exists(prof):
         try:
             traffic = json.load(open(prof)).get("dram_bytes_per_launch")
         except Exception:
             traffic = None
     if int8:
-        ach = float(np.mean([o / (t * 1e-3) / 1e12 for o, t in zip(tops, per_mode)]))
+        # algorithmic INT8 work of one launch: the 28 slice products of the
+        # Ozaki scheme over the unpadded contraction, 2 x 28 x W x prod(dims)
+        # (the padded tiles the kernel actually issues are reported beside it)
+        alg_ops = 2.0 * 28.0 * W * float(np.prod(dims))
+        ach = float(np.mean([alg_ops / (t * 1e-3) / 1e12 for t in per_mode]))
+        executed = float(np.mean([o / (t * 1e-3) / 1e12 for o, t in zip(tops, per_mode)]))
         roofline = {"bound": "tensor", "achieved": ach, "peak": peak_i8.value, "unit": "TOPS",
                     "frac": ach / peak_i8.value, "traffic": traffic,
                     "kernel": f"mttkrp_ozaki_kernel (INT8 tcgen05, 7x7 Ozaki slices, 28 products) "
                               f"+ Lo slicing + split reduce (cals_mttkrp), W={W}, {name}",
-                    "achieved_counts": "executed INT8 ops: 2 x 28 slice products x padded "
-                                       "M x W x K tiles per slab",
+                    "achieved_counts": "algorithmic INT8 ops per launch: 2 x 28 slice products "
+                                       "x W x prod(dims) (unpadded)",
+                    "executed_tops": executed,
+                    "executed_counts": "INT8 ops the kernel issues: 2 x 28 x padded M x W x K "
+                                       "tiles per slab (64-row / 128-column / 32-deep tiles)",
                     "peak_source": "cals_int8_peak_probe: tcgen05.mma kind::i8 M128 N256 K32 on "
                                    "all SMs, measured live (MEASURED_PEAKS.json has no INT8 entry)",
                     "fp64_equivalent": {"tflops": fp64_eq, "dmma_peak_tflops": peak.value,

@@ -403,6 +403,7 @@ __device__ __forceinline__ int plan_scan(int v, int* wtot, int* total) {
 // widths, move lengths, retirement order) are block scans, and only the FIFO
 // admission with head-of-line blocking runs on one thread.
 __global__ void __launch_bounds__(kPlanThreads, 1) engine_plan_kernel(EngState* st) {
+  griddep_wait();  // launched with PDL (launch_dep): predecessors complete
   if (st->done) return;
   __shared__ int wtot[32];
   __shared__ int s_new_w, s_new_n, s_retired, s_moves, s_pre;
@@ -563,6 +564,7 @@ __global__ void __launch_bounds__(kPlanThreads, 1) engine_plan_kernel(EngState* 
 // One block per (mode, row): snapshot the old active row, then apply the move
 // list -> no in-place hazards.
 __global__ void engine_move_kernel(EngState* st) {
+  griddep_wait();  // launched with PDL (launch_dep): predecessors complete
   const int total = st->move_elems;
   if (total == 0) return;
   extern __shared__ __align__(16) double row[];
@@ -592,7 +594,6 @@ __global__ void engine_move_kernel(EngState* st) {
       }
       const int r = e - st->mv_pre[lo];
       const int k = st->mv_model[lo];
-      const int R = st->rank[k];
       const long long po = st->pool_off[(long long)k * N + n] + r * st->dims[n] + i;
       if (snap && st->mv_kind[lo] != kMoveKeep) continue;
       switch (st->mv_kind[lo]) {
@@ -692,6 +693,7 @@ struct Engine {
   // solve(n), i.e. concurrently with the fused MTTKRP of mode n.
   bool split = false;
   UpdArgs ua{};
+  int lo_target = -1;  // mode whose contraction takes its Lo slices from solve(0)
   PrepKernel prep_kernel = nullptr;
   SolveKernel solve_kernel = nullptr, solve_last_kernel = nullptr;
   size_t solve_smem = 0;
@@ -973,6 +975,7 @@ static int engine_create(Tensor* t, int capacity, int n_models, const int* ranks
   }
   ua.ld = e->ld;
   ua.order = N;
+  ua.lo_src = -1;
   if (e->split) {
     split_kernels_for(e->upd_rb, &e->prep_kernel, &e->solve_kernel, &e->solve_last_kernel,
                       &e->solve_smem);
@@ -1133,14 +1136,14 @@ static int enqueue_mode_mttkrp(Engine* e, int n, cudaStream_t stream) {
       // M1 = sum_k A2[k] (sum_i X[i,:,k] A0(new)[i]); slab products = Z[j + I1 k]
       rc = launch_contraction(t, e->tree_plan, 1, F[0], t.dims[0], ld, F[2], ld, 0, wptr, cap, Mo,
                               ld, e->d_ws, e->tree_variant, stream, e->d_partial, ld, t.dims[1],
-                              oz_ws, oz_bytes);
+                              oz_ws, oz_bytes, n == e->lo_target);
     } else if (e->tree == kTreeZ && n == 2) {
       // M2 = Z x_j A1(new): A0 unchanged since Z was formed
       rc = launch_partial_ttv(e->d_partial, ld, t.dims[1], t.dims[2], 0, t.dims[1], F[1], ld, 0,
                               wptr, cap, t.dims[2], Mo, ld, sms, stream);
     } else {
       rc = launch_mttkrp(t, n, fs, 0, wptr, cap, Mo, ld, e->d_ws, e->ws_bytes, e->variants[n],
-                         stream);
+                         stream, n == e->lo_target);
     }
     if (rc) return rc;
   }
@@ -1155,10 +1158,9 @@ static int enqueue_mode_update(Engine* e, int n, cudaStream_t stream) {
 }
 
 static int enqueue_plan(Engine* e, cudaStream_t stream) {
-  engine_plan_kernel<<<1, kPlanThreads, 0, stream>>>(e->d_st);
-  CALS_CUDA_TRY(cudaGetLastError());
-  engine_move_kernel<<<e->move_grid, 256, e->move_smem, stream>>>(e->d_st);
-  CALS_CUDA_TRY(cudaGetLastError());
+  CALS_CUDA_TRY(launch_dep(engine_plan_kernel, dim3(1), dim3(kPlanThreads), 0, stream, e->d_st));
+  CALS_CUDA_TRY(launch_dep(engine_move_kernel, dim3(e->move_grid), dim3(256), e->move_smem, stream,
+                           e->d_st));
   return kOk;
 }
 
@@ -1181,7 +1183,7 @@ static int enqueue_line_search(Engine* e, cudaStream_t stream) {
 }
 
 // CALS_PDL=0 disables programmatic dependent launches (A/B measurements)
-static bool pdl_enabled() {
+bool pdl_enabled() {
   static const bool on = [] {
     const char* v = getenv("CALS_PDL");
     return !v || atoi(v) != 0;
@@ -1352,6 +1354,50 @@ static int engine_capture(Engine* e, cudaStream_t stream) {
 
 // Run every queued model to retirement.  `pool` must already hold the
 // starting factors (per model, per mode, row-major I_n x R_k).
+// Lo-slice fusion (UpdArgs::lo_src): when the first contraction after mode 0
+// takes F[0] (just solved) as its Lo operand and runs on the INT8 path, the
+// mode-0 solve kernel writes that contraction's Lo slices, exponents and
+// unit counter, and the contraction skips its slicing kernel (one launch and
+// one pass over the factor less per iteration; identical slices).  Only on the
+// plain split-update path (no line search / NNLS, whose extra contractions
+// share the workspace) with single-chunk mode-0 solves.  CALS_FUSE_LO=0
+// disables it.
+static void setup_lo_fusion(Engine* e) {
+  e->lo_target = -1;
+  e->ua.lo_src = -1;
+  const char* env = getenv("CALS_FUSE_LO");
+  if (env && atoi(env) == 0) return;
+  if (!e->split || e->h_st.nonneg || e->h_st.ls_enabled || e->order != 3 || e->nch[0] != 1)
+    return;
+  Tensor& t = *e->t;
+  for (int n = 1; n < e->order; ++n) {
+    if ((e->tree == kTreeY && n == 1) || (e->tree == kTreeZ && n == 2)) continue;  // TTV
+    const ModePlan* p;
+    void* ws;
+    int key = n;
+    if (e->tree == kTreeZ && n == 1) {  // Z = X x_1 A0(new): Lo = F[0]
+      p = &e->tree_plan;
+      ws = reinterpret_cast<char*>(e->d_ws) + tree_ws_offset(e->tree_plan, e->ld);
+    } else {
+      p = &t.plans[n];
+      if (!p->lo_direct() || p->lo_modes[0] != 0) return;
+      ws = mttkrp_oz_ws(t, n, e->ld, e->d_ws, e->ws_bytes);
+    }
+    if (!ws || !ozaki_ready(t, *p, key)) return;
+    const OzLoLayout l = ozaki_lo_layout(*p, t.dims[0], e->capacity, ws);
+    UpdArgs& ua = e->ua;
+    ua.lo_ls = l.ls;
+    ua.lo_cex = l.cex;
+    ua.lo_queue = l.queue;
+    ua.lo_stride = l.slice_stride;
+    ua.lo_Kp = l.Kp;
+    ua.lo_Dp = l.Dp;
+    ua.lo_src = 0;
+    e->lo_target = n;
+    return;
+  }
+}
+
 static int engine_run(Engine* e, double tol, int max_iterations, double sqnorm, int use_graph,
                       cudaStream_t stream, int* iterations_out) {
   CALS_CHECK(max_iterations >= 1, kErrInvalid, "max_iterations must be >= 1");
@@ -1364,9 +1410,11 @@ static int engine_run(Engine* e, double tol, int max_iterations, double sqnorm, 
   }
   rc = engine_prepare_slices(e, stream);
   if (rc) return rc;
+  setup_lo_fusion(e);
   // initial admission
-  engine_plan_kernel<<<1, kPlanThreads, 0, stream>>>(e->d_st);
-  engine_move_kernel<<<e->move_grid, 256, e->move_smem, stream>>>(e->d_st);
+  CALS_CUDA_TRY(launch_dep(engine_plan_kernel, dim3(1), dim3(kPlanThreads), 0, stream, e->d_st));
+  CALS_CUDA_TRY(launch_dep(engine_move_kernel, dim3(e->move_grid), dim3(256), e->move_smem, stream,
+                           e->d_st));
   CALS_CUDA_TRY(cudaGetLastError());
   if (use_graph) {
     rc = engine_capture(e, stream);
@@ -1826,6 +1874,9 @@ int cals_engine_begin(cals_engine* e, double tol, int max_iterations, double sqn
   }
   rc = engine_prepare_slices(g, s);
   if (rc) return rc;
+  // the step-wise driver reduces partial MTTKRPs between the calls: no fusion
+  g->lo_target = -1;
+  g->ua.lo_src = -1;
   return enqueue_plan(g, s);  // initial admission
 }
 

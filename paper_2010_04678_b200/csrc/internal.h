@@ -10,6 +10,7 @@
 #include <atomic>
 #include <memory>
 #include <string>
+#include <utility>
 #include <vector>
 
 #include "common.cuh"
@@ -70,6 +71,29 @@ void tensor_destroy(Tensor* t);
 int check_current_device(const Tensor& t);
 int tensor_sqnorm(Tensor* t, cudaStream_t stream, double* out);
 ModePlan make_plan(const Tensor& t, int mode);
+// Programmatic dependent launch (PDL): every kernel of the engine's
+// iteration is launched with programmatic stream serialization, so its launch
+// overlaps the tail of the kernel before it; each such kernel calls
+// griddep_wait() before it touches anything its predecessors wrote (at its
+// very top unless noted), so stream order is preserved transitively.
+// CALS_PDL=0 disables it (A/B measurements).
+bool pdl_enabled();
+template <typename... P, typename... A>
+inline cudaError_t launch_dep(void (*k)(P...), dim3 grid, dim3 block, size_t smem,
+                              cudaStream_t stream, A&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = stream;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, k, std::forward<A>(args)...);
+}
+
 int plan_splits(const ModePlan& view);  // shape-only q-split count of a view
 
 // MTTKRP variants ------------------------------------------------------------
@@ -95,7 +119,11 @@ struct FactorSet {
 // sizes the grid.
 int launch_mttkrp(Tensor& t, int mode, const FactorSet& f, int width, const int* width_ptr,
                   long long cap, double* out, long long ldo, double* workspace,
-                  size_t workspace_bytes, int variant, cudaStream_t stream);
+                  size_t workspace_bytes, int variant, cudaStream_t stream,
+                  bool lo_sliced = false);
+// The Ozaki workspace launch_mttkrp carves for `mode` out of `workspace`
+// (nullptr when the mode does not run on the INT8 path or it does not fit).
+void* mttkrp_oz_ws(Tensor& t, int mode, long long ld, void* workspace, size_t workspace_bytes);
 
 // Lower level: one contraction on an arbitrary 3-D view plan `p` of the tensor
 // with explicit Lo [lrows][lo_ld] / Hi [Dq][hi_ld] operands.  map_key caches
@@ -108,7 +136,7 @@ int launch_contraction(Tensor& t, const ModePlan& p, int map_key, const double* 
                        int width, const int* width_ptr, long long cap, double* out, long long ldo,
                        double* part, int variant, cudaStream_t stream, double* side = nullptr,
                        long long side_ld = 0, long long side_qstride = 0, void* oz_ws = nullptr,
-                       size_t oz_ws_bytes = 0);
+                       size_t oz_ws_bytes = 0, bool lo_sliced = false);
 
 // Ozaki-sliced INT8 tensor-core contraction (ozaki.cu) ------------------------
 bool ozaki_enabled();                       // CALS_MTTKRP=dmma disables it
@@ -124,12 +152,29 @@ int ozaki_prepare(Tensor& t, const ModePlan& p, int key, cudaStream_t stream,
                   bool validate = true);
 int ozaki_validate(Tensor& t, int key, cudaStream_t stream);
 void ozaki_release(Tensor& t);
+// Whether a contraction of view `p` (slices under `key`) will run on the INT8
+// path: eligible, slices prepared and checked.
+bool ozaki_ready(Tensor& t, const ModePlan& p, int key);
+// Where the per-call Lo slices of a contraction live in its Ozaki workspace:
+// ls[7][cap_pad][Kp] (column c of Lo as a p-contiguous row), cex[c], and the
+// work-unit counter.  A producer that writes them itself (the split update's
+// solve kernel, update2.cu) lets the contraction skip its slicing kernel
+// (lo_sliced = true).
+struct OzLoLayout {
+  uint8_t* ls = nullptr;
+  int* cex = nullptr;
+  int* queue = nullptr;
+  long long slice_stride = 0;  // cap_pad * Kp
+  int Kp = 0;
+  int Dp = 0;                  // Lo rows sliced (the rest of Kp is zero)
+};
+OzLoLayout ozaki_lo_layout(const ModePlan& p, long long lrows, long long cap, void* oz_ws);
 int launch_contraction_ozaki(Tensor& t, const ModePlan& p, int key, const double* lo,
                              long long lrows, long long lo_ld, const double* hi, long long hi_ld,
                              int width, const int* width_ptr, long long cap, double* out,
                              long long ldo, double* part, void* oz_ws, size_t oz_ws_bytes,
                              cudaStream_t stream, double* side, long long side_ld,
-                             long long side_qstride);
+                             long long side_qstride, bool lo_sliced = false);
 
 // out[row][c] = sum over the reduced index of P[a + Da*b][c] * F[idx][c]
 // (reduce_b: rows a < rows_out, sum b < Db with F[b]; else rows b, sum a < La

@@ -335,10 +335,10 @@ static cudaError_t launch_variant(dim3 grid, const CUtensorMap& a, const CUtenso
   });
   if (cfg != cudaSuccess) return cfg;
   if (kc)
-    mttkrp_dmma_kernel<MI, NI, WM, WN, true><<<grid, C::kThreads, smem, stream>>>(a, b, args);
-  else
-    mttkrp_dmma_kernel<MI, NI, WM, WN, false><<<grid, C::kThreads, smem, stream>>>(a, b, args);
-  return cudaGetLastError();
+    return launch_dep(mttkrp_dmma_kernel<MI, NI, WM, WN, true>, grid, dim3(C::kThreads), smem,
+                      stream, a, b, args);
+  return launch_dep(mttkrp_dmma_kernel<MI, NI, WM, WN, false>, grid, dim3(C::kThreads), smem,
+                    stream, a, b, args);
 }
 
 template <int MI, int NI, int WM, int WN>
@@ -440,6 +440,7 @@ __global__ void fill_kernel(double* p, long long n, double v) {
 __global__ void split_reduce_kernel(const double* __restrict__ part, long long part_stride, int S,
                                     int M, long long ldp, const int* width_ptr, int width,
                                     double* __restrict__ out, long long ldo) {
+  griddep_wait();  // launched with PDL (launch_dep): predecessors complete
   griddep_launch_dependents();  // the next kernel may start its prologue
   const int W = width_ptr ? *width_ptr : width;
   const int hw = (W + 1) >> 1;  // column pairs
@@ -482,7 +483,7 @@ size_t mttkrp_workspace_bytes(const Tensor& t, int mode, long long cap) {
 
 int launch_mttkrp(Tensor& t, int mode, const FactorSet& f, int width, const int* width_ptr,
                   long long cap, double* out, long long ldo, double* workspace,
-                  size_t workspace_bytes, int variant, cudaStream_t stream) {
+                  size_t workspace_bytes, int variant, cudaStream_t stream, bool lo_sliced) {
   CALS_CHECK(mode >= 0 && mode < t.order, kErrInvalid, "mode out of range");
   const ModePlan& p = t.plans[mode];
   CALS_CHECK(f.ld % 2 == 0 && f.ld >= cap, kErrInvalid, "factor leading dimension must be even");
@@ -562,7 +563,20 @@ int launch_mttkrp(Tensor& t, int mode, const FactorSet& f, int width, const int*
     }
   }
   return launch_contraction(t, p, mode, lo, lrows, lo_ld, hi, hi_ld, width, width_ptr, cap, out,
-                            ldo, part, variant, stream, nullptr, 0, 0, oz_ws, oz_bytes);
+                            ldo, part, variant, stream, nullptr, 0, 0, oz_ws, oz_bytes, lo_sliced);
+}
+
+void* mttkrp_oz_ws(Tensor& t, int mode, long long ld, void* workspace, size_t workspace_bytes) {
+  const ModePlan& p = t.plans[mode];
+  if (!ozaki_eligible(p)) return nullptr;
+  size_t off = 0;  // the carve of launch_mttkrp
+  if (p.S > 1) off += size_t(p.S) * size_t(p.M) * size_t(ld) * 8;
+  if (!p.lo_direct()) off += size_t(p.Dp) * size_t(ld) * 8;
+  if (!p.hi_direct()) off += size_t(std::max<long long>(p.Dq, 1)) * size_t(ld) * 8;
+  char* base = reinterpret_cast<char*>(workspace);
+  char* o = reinterpret_cast<char*>((reinterpret_cast<uintptr_t>(base + off) + 255) & ~uintptr_t(255));
+  if (o + ozaki_ws_bytes(p, ld) > base + workspace_bytes) return nullptr;
+  return o;
 }
 
 int launch_contraction(Tensor& t, const ModePlan& p, int map_key, const double* lo,
@@ -570,7 +584,7 @@ int launch_contraction(Tensor& t, const ModePlan& p, int map_key, const double* 
                        int width, const int* width_ptr, long long cap, double* out, long long ldo,
                        double* part, int variant, cudaStream_t stream, double* side,
                        long long side_ld, long long side_qstride, void* oz_ws,
-                       size_t oz_ws_bytes) {
+                       size_t oz_ws_bytes, bool lo_sliced) {
   static const bool dbg = getenv("CALS_DEBUG_OZ") != nullptr;
   if (dbg)
     fprintf(stderr, "[oz] contraction key=%d role=%d M=%lld Dp=%lld Dq=%lld S=%d oz_ws=%p elig=%d\n",
@@ -578,7 +592,7 @@ int launch_contraction(Tensor& t, const ModePlan& p, int map_key, const double* 
   if (oz_ws && ozaki_eligible(p)) {
     const int rc = launch_contraction_ozaki(t, p, map_key, lo, lrows, lo_ld, hi, hi_ld, width,
                                             width_ptr, cap, out, ldo, part, oz_ws, oz_ws_bytes,
-                                            stream, side, side_ld, side_qstride);
+                                            stream, side, side_ld, side_qstride, lo_sliced);
     if (dbg) fprintf(stderr, "[oz]   ozaki rc=%d\n", rc);
     if (rc != kErrUnsupported) return rc;  // unsupported = slices not prepared: DMMA below
   }
@@ -640,9 +654,9 @@ int launch_contraction(Tensor& t, const ModePlan& p, int map_key, const double* 
   if (p.S > 1) {
     const long long pairs = p.M * ((cap + 1) / 2);
     const int blocks = (int)std::max<long long>(1, std::min<long long>(sms * 8, (pairs + 255) / 256));
-    split_reduce_kernel<<<blocks, 256, 0, stream>>>(part, a.part_stride, p.S, (int)p.M, lo_ld,
-                                                    width_ptr, width, out, ldo);
-    CALS_CUDA_TRY(cudaGetLastError());
+    CALS_CUDA_TRY(launch_dep(split_reduce_kernel, dim3(blocks), dim3(256), 0, stream,
+                             (const double*)part, (long long)a.part_stride, p.S, (int)p.M,
+                             (long long)lo_ld, width_ptr, width, out, (long long)ldo));
   }
   return kOk;
 }
@@ -658,6 +672,7 @@ __global__ void partial_ttv_kernel(const double* __restrict__ P, long long ld, l
                                    const double* __restrict__ F, long long ldf,
                                    const int* width_ptr, int width, long long rows_out,
                                    double* __restrict__ out, long long ldo) {
+  griddep_wait();  // launched with PDL (launch_dep): predecessors complete
   griddep_launch_dependents();  // the next kernel may start its prologue
   const int W = width_ptr ? *width_ptr : width;
   const long long n = (reduce_b ? rows_out : (rows_out + 3) / 4) * W;
@@ -750,6 +765,7 @@ __global__ void __launch_bounds__(512) partial_ttv_split_kernel(const double* __
                                          long long ldf, const int* width_ptr, int width,
                                          long long rows_out, double* __restrict__ out,
                                          long long ldo) {
+  griddep_wait();  // launched with PDL (launch_dep): predecessors complete
   griddep_launch_dependents();  // the next kernel may start its prologue
   extern __shared__ double red[];  // [G][4][32]
   const int W = width_ptr ? *width_ptr : width;
@@ -827,16 +843,15 @@ int launch_partial_ttv(const double* P, long long ld, long long Da, long long Db
     const long long G = std::min<long long>({16, 65536 / std::max<long long>(1, threads), La / 8});
     if (G >= 2) {
       const dim3 grid((unsigned)((cap + 31) / 32), (unsigned)((rows_out + 3) / 4));
-      partial_ttv_split_kernel<<<grid, dim3(32, (unsigned)G), size_t(G) * 128 * 8, stream>>>(
-          P, ld, Da, La, F, ldf, width_ptr, width, rows_out, out, ldo);
-      CALS_CUDA_TRY(cudaGetLastError());
+      CALS_CUDA_TRY(launch_dep(partial_ttv_split_kernel, grid, dim3(32, (unsigned)G),
+                               size_t(G) * 128 * 8, stream, P, ld, Da, La, F, ldf, width_ptr,
+                               width, rows_out, out, ldo));
       return kOk;
     }
   }
   const int blocks = (int)std::max<long long>(1, std::min<long long>(sms * 16, (n + 255) / 256));
-  partial_ttv_kernel<<<blocks, 256, 0, stream>>>(P, ld, Da, Db, reduce_b, La, F, ldf, width_ptr,
-                                                 width, rows_out, out, ldo);
-  CALS_CUDA_TRY(cudaGetLastError());
+  CALS_CUDA_TRY(launch_dep(partial_ttv_kernel, dim3(blocks), dim3(256), 0, stream, P, ld, Da, Db,
+                           reduce_b, La, F, ldf, width_ptr, width, rows_out, out, ldo));
   return kOk;
 }
 

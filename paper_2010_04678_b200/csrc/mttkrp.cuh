@@ -115,6 +115,7 @@ __global__ void __launch_bounds__(TileCfg<MI, NI, WM, WN>::kThreads, 2)
   uint64_t* full = reinterpret_cast<uint64_t*>(smem_raw + STAGES * C::kStageBytes);
   uint64_t* empty = full + STAGES;
 
+  griddep_wait();  // launched with PDL (launch_dep): predecessors complete
   const int W = args.width_ptr ? *args.width_ptr : args.width;
   if (W <= 0) return;
   const int tm = (args.M + BM - 1) / BM;

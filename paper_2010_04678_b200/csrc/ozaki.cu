@@ -141,6 +141,7 @@ __global__ void oz_slice_cols_kernel(const double* __restrict__ lo, long long ld
   __shared__ double tile[32][33];
   __shared__ double red[8][33];
   __shared__ int ex[32];
+  griddep_wait();  // launched with PDL (launch_dep): predecessors complete
   // the contraction kernel that follows claims its work units from *queue
   if (blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0) *queue = 0;
   const int W = width_ptr ? *width_ptr : width;
@@ -205,6 +206,7 @@ __global__ void __launch_bounds__(256) oz_slice_cols_all_kernel(
   extern __shared__ double ctile[];  // [Kp][33]
   __shared__ double red[8][33];
   __shared__ int ex[32];
+  griddep_wait();  // launched with PDL (launch_dep): predecessors complete
   if (blockIdx.x == 0 && threadIdx.x == 0) *queue = 0;
   const int W = width_ptr ? *width_ptr : width;
   const int c0 = blockIdx.x * 32;
@@ -466,6 +468,28 @@ int ozaki_prepare(Tensor& t, const ModePlan& p, int key, cudaStream_t stream, bo
   return kOk;
 }
 
+bool ozaki_ready(Tensor& t, const ModePlan& p, int key) {
+  if (!ozaki_eligible(p)) return false;
+  std::lock_guard<std::mutex> lk(t.mu);
+  auto it = t.oz.find(key);
+  return it != t.oz.end() && !it->second.flag && it->second.M == p.M && it->second.Dq == p.Dq &&
+         it->second.Dp == p.Dp;
+}
+
+OzLoLayout ozaki_lo_layout(const ModePlan& p, long long lrows, long long cap, void* oz_ws) {
+  OzLoLayout l;
+  const long long cap_pad = (cap + BMC - 1) / BMC * BMC;
+  l.Kp = (int)kp_of(p.Dp);
+  l.Dp = (int)std::min<long long>(lrows, p.Dp);
+  l.slice_stride = cap_pad * l.Kp;
+  l.ls = reinterpret_cast<uint8_t*>(oz_ws);
+  l.cex = reinterpret_cast<int*>(
+      (reinterpret_cast<uintptr_t>(l.ls + size_t(kSlices) * cap_pad * l.Kp) + 255) &
+      ~uintptr_t(255));
+  l.queue = l.cex + cap_pad;  // inside the cap_pad * 8 bytes reserved after the slices
+  return l;
+}
+
 void ozaki_release(Tensor& t) {
   for (auto& kv : t.oz) {
     cudaFreeAsync(kv.second.xs, 0);
@@ -480,7 +504,7 @@ int launch_contraction_ozaki(Tensor& t, const ModePlan& p, int key, const double
                              int width, const int* width_ptr, long long cap, double* out,
                              long long ldo, double* part, void* oz_ws, size_t oz_ws_bytes,
                              cudaStream_t stream, double* side, long long side_ld,
-                             long long side_qstride) {
+                             long long side_qstride, bool lo_sliced) {
   OzSlices o;
   {
     std::lock_guard<std::mutex> lk(t.mu);
@@ -493,16 +517,19 @@ int launch_contraction_ozaki(Tensor& t, const ModePlan& p, int key, const double
              "Ozaki workspace too small");
   CALS_CHECK(p.S == 1 || part != nullptr, kErrInvalid, "split-K needs a partial buffer");
   const long long cap_pad = (cap + BMC - 1) / BMC * BMC;
-  uint8_t* ls = reinterpret_cast<uint8_t*>(oz_ws);
-  int* cex = reinterpret_cast<int*>(
-      (reinterpret_cast<uintptr_t>(ls + size_t(kSlices) * cap_pad * o.Kp) + 255) & ~uintptr_t(255));
-  int* queue = cex + cap_pad;  // inside the cap_pad * 8 bytes reserved after the slices
+  const OzLoLayout lay = ozaki_lo_layout(p, lrows, cap, oz_ws);
+  uint8_t* ls = lay.ls;
+  int* cex = lay.cex;
+  int* queue = lay.queue;
   const int sms = sm_count(t.device);
 
   // the one-block-per-column-block kernel wins when there are enough column
   // blocks to fill the GPU (c2: 66 -> 10.6 vs 12.7 us); narrow pools (c3's
   // 10) keep the p-chunked grid (9.0 vs 11.4 us)
-  if (o.Kp <= kColsAllMaxKp && (cap + 31) / 32 >= 32) {
+  if (lo_sliced) {
+    // the kernel that produced Lo also wrote its slices, exponents and the
+    // zeroed unit counter (ozaki_lo_layout)
+  } else if (o.Kp <= kColsAllMaxKp && (cap + 31) / 32 >= 32) {
     const size_t smem = size_t(o.Kp) * 33 * 8;
     static std::once_flag once;
     static cudaError_t attr = cudaSuccess;
@@ -512,14 +539,14 @@ int launch_contraction_ozaki(Tensor& t, const ModePlan& p, int key, const double
                                   kColsAllMaxKp * 33 * 8);
     });
     CALS_CUDA_TRY(attr);
-    oz_slice_cols_all_kernel<<<(unsigned)((cap + 31) / 32), 256, smem, stream>>>(
-        lo, lo_ld, (int)std::min<long long>(lrows, p.Dp), (int)o.Kp, width_ptr, width, cap_pad,
-        ls, cex, queue);
+    CALS_CUDA_TRY(launch_dep(oz_slice_cols_all_kernel, dim3((unsigned)((cap + 31) / 32)), dim3(256),
+                             smem, stream, lo, lo_ld, (int)std::min<long long>(lrows, p.Dp),
+                             (int)o.Kp, width_ptr, width, (long long)cap_pad, ls, cex, queue));
   } else {
-    oz_slice_cols_kernel<<<dim3((unsigned)((cap + 31) / 32), (unsigned)(o.Kp / 32)), 256, 0,
-                           stream>>>(
-        lo, lo_ld, (int)std::min<long long>(lrows, p.Dp), (int)o.Kp, width_ptr, width, cap_pad,
-        ls, cex, queue);
+    CALS_CUDA_TRY(launch_dep(oz_slice_cols_kernel,
+                             dim3((unsigned)((cap + 31) / 32), (unsigned)(o.Kp / 32)), dim3(256), 0,
+                             stream, lo, lo_ld, (int)std::min<long long>(lrows, p.Dp), (int)o.Kp,
+                             width_ptr, width, (long long)cap_pad, ls, cex, queue));
   }
   CALS_CUDA_TRY(cudaGetLastError());
 
@@ -595,16 +622,19 @@ int launch_contraction_ozaki(Tensor& t, const ModePlan& p, int key, const double
       ((cap + BMC - 1) / BMC) * (mt.tm_full + (mt.rem_rows ? 1 : 0)) * (long long)p.S;
   dim3 grid((unsigned)std::max<long long>(1, std::min<long long>(units, sms)));
   if (side)
-    mttkrp_ozaki_kernel<true><<<grid, kThreads, kSmemBytes, stream>>>(o.map, mapL, o.rmap, a);
+    CALS_CUDA_TRY(launch_dep(mttkrp_ozaki_kernel<true>, grid, dim3(kThreads), kSmemBytes, stream,
+                             o.map, mapL, o.rmap, a));
   else
-    mttkrp_ozaki_kernel<false><<<grid, kThreads, kSmemBytes, stream>>>(o.map, mapL, o.rmap, a);
+    CALS_CUDA_TRY(launch_dep(mttkrp_ozaki_kernel<false>, grid, dim3(kThreads), kSmemBytes, stream,
+                             o.map, mapL, o.rmap, a));
   CALS_CUDA_TRY(cudaGetLastError());
   if (p.S > 1) {
     const long long pairs = p.M * ((cap + 1) / 2);
     const int blocks =
         (int)std::max<long long>(1, std::min<long long>(sms * 8, (pairs + 255) / 256));
-    split_reduce_kernel<<<blocks, 256, 0, stream>>>(part, a.part_stride, p.S, (int)p.M, lo_ld,
-                                                    width_ptr, width, out, ldo);
+    CALS_CUDA_TRY(launch_dep(split_reduce_kernel, dim3(blocks), dim3(256), 0, stream,
+                             (const double*)part, (long long)a.part_stride, p.S, (int)p.M,
+                             (long long)lo_ld, width_ptr, width, out, (long long)ldo));
     CALS_CUDA_TRY(cudaGetLastError());
   }
   return kOk;

@@ -255,6 +255,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint32_t* tmem_base_slot = reinterpret_cast<uint32_t*>(uring + kUnitRing);
 
   if ((smem_u32(smem) & 1023u) != 0) __trap();
+  griddep_wait();  // launched with PDL (launch_dep): predecessors complete
   const int W = args.width_ptr ? *args.width_ptr : args.width;
   if (W <= 0) return;
   const int tn = (W + BMC - 1) / BMC;

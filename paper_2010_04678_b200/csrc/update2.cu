@@ -1,6 +1,7 @@
 // Split per-model update kernels (design: update2.cuh).
 #include "update.cuh"
 #include "update2.cuh"
+#include "ozaki.cuh"
 
 namespace cals {
 
@@ -207,31 +208,44 @@ __device__ __forceinline__ void finish_model(const UpdArgs& a, int k, double msq
     decide_model(st, k, e);
 }
 
+// One factor row: A = M H^-1 with H = U^T U (dpotrs: forward substitution
+// with U^T, then back substitution with U; reciprocal diagonal).  The k loops
+// stay rolled: the row lives in registers and shifts down one slot per step
+// (register rotation), so every step reads its operands at static indices.
+// Us / Vs hold U and U^T pre-shifted by the solve kernel: Us[k][j] =
+// U[k][k+1+j], Vs[k][j] = U^T[k][k-1-j], zero past the triangle.  Each
+// element sees exactly the unrolled dtrsm sequence x_c = fma(-u, y_k, x_c),
+// k ascending (forward) / descending (back); the slots past the triangle only
+// carry unused values.  A fully unrolled per-rank solve is ~R^2 instructions
+// of straight-line code fetched cold by every CTA (ncu: no_instruction was the
+// top stall); this body is ~6 R instructions.
 template <int R>
 __device__ __forceinline__ void solve_row_exact(double* __restrict__ xs,
-                                                const double* __restrict__ U,
-                                                const double* __restrict__ V,
+                                                const double* __restrict__ Us,
+                                                const double* __restrict__ Vs,
                                                 const double* __restrict__ invd) {
-  constexpr int RP = R + (R & 1);
-  double x[R];
+  constexpr int RS = R + (R & 1);
+  double r[R];
 #pragma unroll
-  for (int c = 0; c < R; ++c) x[c] = xs[c];
-#pragma unroll
+  for (int c = 0; c < R; ++c) r[c] = xs[c];
+#pragma unroll 1
   for (int k = 0; k < R; ++k) {
-    const double yk = x[k] * invd[k];
-    x[k] = yk;
+    const double yk = r[0] * invd[k];
+    xs[k] = yk;
+    const double* u = Us + k * RS;
 #pragma unroll
-    for (int c = k + 1; c < R; ++c) x[c] = fma(-U[k * RP + c], yk, x[c]);
+    for (int j = 0; j + 1 < R; ++j) r[j] = fma(-u[j], yk, r[j + 1]);
   }
 #pragma unroll
+  for (int j = 0; j < R; ++j) r[j] = xs[R - 1 - j];
+#pragma unroll 1
   for (int k = R - 1; k >= 0; --k) {
-    const double xk = x[k] * invd[k];
-    x[k] = xk;
+    const double xk = r[0] * invd[k];
+    xs[k] = xk;
+    const double* v = Vs + k * RS;
 #pragma unroll
-    for (int c = 0; c < k; ++c) x[c] = fma(-V[k * RP + c], xk, x[c]);
+    for (int j = 0; j + 1 < R; ++j) r[j] = fma(-v[j], xk, r[j + 1]);
   }
-#pragma unroll
-  for (int c = 0; c < R; ++c) xs[c] = x[c];
 }
 
 template <int RB, int R = 1>
@@ -315,6 +329,53 @@ __device__ __forceinline__ void tile_gram_tc(const double* __restrict__ X, int P
   }
 }
 
+// Lo-slice fusion (UpdArgs::lo_src): the Ozaki Lo slices of this model's
+// columns [off, off + R) of F[n] -- every row, so only single-chunk solves --
+// exactly as oz_slice_cols_kernel / oz_slice_cols_all_kernel form them: the
+// column maximum over the Dp rows (scale_exp_checked), slice7 per element,
+// zeros for p in [Dp, Kp).  Reads the factor back from global memory (this
+// CTA's own stores, visible after the barrier that precedes the call).
+__device__ __noinline__ void slice_lo_columns(const UpdArgs& a, int n, int off, int R) {
+  __shared__ int ex_s[32];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const double* A = a.F[n] + off;
+  const long long ld = a.ld;
+  const int Dp = a.lo_Dp, Kp = a.lo_Kp;
+  if (blockIdx.x == 0 && tid == 0) *a.lo_queue = 0;  // the contraction's unit counter
+  for (int c = warp; c < R; c += kSolveRows / 32) {
+    double mx = 0.0;
+    for (int p = lane; p < Dp; p += 32) mx = fmax(mx, oz::abs_or_inf(A[(long long)p * ld + c]));
+#pragma unroll
+    for (int o = 16; o; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    if (lane == 0) {
+      const int e = oz::scale_exp_checked(mx);
+      ex_s[c] = e;
+      a.lo_cex[off + c] = e;
+    }
+  }
+  __syncthreads();
+  const int groups = Kp >> 2;  // 4 consecutive p per thread: one 32-bit word per slice
+  for (int idx = tid; idx < R * groups; idx += kSolveRows) {
+    const int c = idx / groups, p0 = (idx - c * groups) * 4;
+    uint32_t w[oz::kSlices];
+#pragma unroll
+    for (int s = 0; s < oz::kSlices; ++s) w[s] = 0u;
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int p = p0 + u;
+      const double v = p < Dp ? A[(long long)p * ld + c] : 0.0;
+      uint8_t sl[oz::kSlices];
+      oz::slice7(v, ex_s[c], sl);
+#pragma unroll
+      for (int s = 0; s < oz::kSlices; ++s) w[s] |= uint32_t(sl[s]) << (8 * u);
+    }
+    uint8_t* dst = a.lo_ls + size_t(off + c) * Kp + p0;
+#pragma unroll
+    for (int s = 0; s < oz::kSlices; ++s)
+      *reinterpret_cast<uint32_t*>(dst + size_t(s) * a.lo_stride) = w[s];
+  }
+}
+
 // Shared-memory layout of upd_solve_kernel<RB> (doubles)
 struct SolveSmem {
   int U, V, H, G, invd, X, scr, red, lam, total;
@@ -328,8 +389,8 @@ template <int RB, bool LAST>
 __global__ void __launch_bounds__(kSolveRows, 2) upd_solve_kernel(UpdArgs a, int n, int nch) {
   extern __shared__ __align__(16) double sm[];
   constexpr SolveSmem L(RB);
-  double* U = sm + L.U;         // U (or pinv), pitch RP
-  double* V = sm + L.V;         // U^T, pitch RP
+  double* U = sm + L.U;         // U pre-shifted (or pinv), pitch RP
+  double* V = sm + L.V;         // U^T pre-shifted, pitch RP
   double* Hs = sm + L.H;        // last mode: Hadamard of G_0 .. G_{N-2} (R x R)
   double* Gs = sm + L.G;        // the refreshed Gramian (R x R)
   double* invd = sm + L.invd;   // 1 / U[a][a]
@@ -362,6 +423,10 @@ __global__ void __launch_bounds__(kSolveRows, 2) upd_solve_kernel(UpdArgs a, int
   SOLVE_STAMP(1)
   if (pf == kPrepFailed) {  // failed earlier in this iteration (driver.py:218-219)
     if (LAST && chunk == 0 && tid == 0) finish_model(a, k, 0.0, 0.0, false);
+    if (!LAST && n == a.lo_src) {  // the factor stays: its slices still feed the next contraction
+      griddep_wait();
+      slice_lo_columns(a, n, off, R);
+    }
     return;
   }
   DecideIn din{};
@@ -379,18 +444,20 @@ __global__ void __launch_bounds__(kSolveRows, 2) upd_solve_kernel(UpdArgs a, int
   // U, U^T (or pinv) and, for the last mode, H: written by prep (before)
   {
     const double* src = a.ubuf + 3 * go;
-    for (int idx = tid; idx < R * R; idx += kSolveRows) {
-      const int r = idx / R, c = idx - r * R;
-      const double u = src[idx];
-      if (pf == kPrepChol) {
-        U[r * RP + c] = u;
-        V[r * RP + c] = src[R * R + idx];
-        if (r == c) invd[r] = u;
-      } else {
-        U[idx] = u;  // pinv, pitch R
+    if (pf == kPrepChol) {
+      // pre-shifted rows for the rotation solve (solve_row_exact)
+      for (int idx = tid; idx < R * RP; idx += kSolveRows) {
+        const int r = idx / RP, j = idx - r * RP;
+        const int cu = r + 1 + j, cv = r - 1 - j;
+        U[idx] = cu < R ? src[r * R + cu] : 0.0;
+        V[idx] = cv >= 0 ? src[R * R + r * R + cv] : 0.0;
       }
-      if (LAST) Hs[idx] = src[2 * R * R + idx];
+      for (int r = tid; r < R; r += kSolveRows) invd[r] = src[r * R + r];
+    } else {
+      for (int idx = tid; idx < R * R; idx += kSolveRows) U[idx] = src[idx];  // pinv, pitch R
     }
+    if (LAST)
+      for (int idx = tid; idx < R * R; idx += kSolveRows) Hs[idx] = src[2 * R * R + idx];
   }
   // The reference checks the whole M block before touching the factor
   // (als.py:84-85): every chunk scans all of it (one chunk at <= 256 rows),
@@ -435,6 +502,7 @@ __global__ void __launch_bounds__(kSolveRows, 2) upd_solve_kernel(UpdArgs a, int
       a.failed[k] = 1;
       if (LAST) finish_model(a, k, 0.0, 0.0, false);
     }
+    if (!LAST && n == a.lo_src) slice_lo_columns(a, n, off, R);
     return;
   }
   int sbad = 0;
@@ -545,7 +613,10 @@ __global__ void __launch_bounds__(kSolveRows, 2) upd_solve_kernel(UpdArgs a, int
   __syncthreads();  // Gs final
   for (int idx = tid; idx < R * R; idx += kSolveRows) Gn[idx] = Gs[idx];
   SOLVE_STAMP(6)
-  if (!LAST) return;
+  if (!LAST) {
+    if (n == a.lo_src) slice_lo_columns(a, n, off, R);
+    return;
+  }
   // fast error (als.py:99-115): sum of the Hadamard of all Gramians, folded
   // ascending -- (G_0 o .. o G_{N-2}) from prep, then o G_{N-1}
   double mpart = 0.0;

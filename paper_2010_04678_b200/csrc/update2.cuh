@@ -59,6 +59,17 @@ struct UpdArgs {
   long long dims[kMaxOrder];
   long long ld;
   int order;
+  // Lo-slice fusion: the solve of mode lo_src (-1: none) also writes the
+  // Ozaki Lo slices of its factor columns for the next INT8 contraction that
+  // takes F[lo_src] as its Lo operand (the oz_slice_cols* arithmetic; that
+  // contraction then skips its slicing kernel).  OzLoLayout in internal.h.
+  uint8_t* lo_ls;
+  int* lo_cex;
+  int* lo_queue;
+  long long lo_stride;  // cap_pad * Kp
+  int lo_Kp;
+  int lo_Dp;
+  int lo_src;
 };
 
 // Shared memory of upd_solve_kernel<RB> (SolveSmem in update2.cu):
