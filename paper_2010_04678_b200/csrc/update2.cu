@@ -333,17 +333,18 @@ __device__ __forceinline__ void tile_gram_tc(const double* __restrict__ X, int P
 // columns [off, off + R) of F[n] -- every row, so only single-chunk solves --
 // exactly as oz_slice_cols_kernel / oz_slice_cols_all_kernel form them: the
 // column maximum over the Dp rows (scale_exp_checked), slice7 per element,
-// zeros for p in [Dp, Kp).  Reads the factor back from global memory (this
-// CTA's own stores, visible after the barrier that precedes the call).
-__device__ __noinline__ void slice_lo_columns(const UpdArgs& a, int n, int off, int R) {
+// zeros for p in [Dp, Kp).  A / ld: the factor block -- the solved rows still
+// in shared memory, or (failure / pinv-redo paths) F[n] in global memory
+// (this CTA's own stores, visible after the barrier that precedes the call).
+__device__ __noinline__ void slice_lo_columns(const UpdArgs& a, int off, int R,
+                                              const double* __restrict__ A, long long ld) {
   __shared__ int ex_s[32];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const double* A = a.F[n] + off;
-  const long long ld = a.ld;
   const int Dp = a.lo_Dp, Kp = a.lo_Kp;
   if (blockIdx.x == 0 && tid == 0) *a.lo_queue = 0;  // the contraction's unit counter
   for (int c = warp; c < R; c += kSolveRows / 32) {
     double mx = 0.0;
+#pragma unroll 4
     for (int p = lane; p < Dp; p += 32) mx = fmax(mx, oz::abs_or_inf(A[(long long)p * ld + c]));
 #pragma unroll
     for (int o = 16; o; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
@@ -425,7 +426,7 @@ __global__ void __launch_bounds__(kSolveRows, 2) upd_solve_kernel(UpdArgs a, int
     if (LAST && chunk == 0 && tid == 0) finish_model(a, k, 0.0, 0.0, false);
     if (!LAST && n == a.lo_src) {  // the factor stays: its slices still feed the next contraction
       griddep_wait();
-      slice_lo_columns(a, n, off, R);
+      slice_lo_columns(a, off, R, a.F[n] + off, a.ld);
     }
     return;
   }
@@ -502,7 +503,7 @@ __global__ void __launch_bounds__(kSolveRows, 2) upd_solve_kernel(UpdArgs a, int
       a.failed[k] = 1;
       if (LAST) finish_model(a, k, 0.0, 0.0, false);
     }
-    if (!LAST && n == a.lo_src) slice_lo_columns(a, n, off, R);
+    if (!LAST && n == a.lo_src) slice_lo_columns(a, off, R, a.F[n] + off, a.ld);
     return;
   }
   int sbad = 0;
@@ -614,7 +615,14 @@ __global__ void __launch_bounds__(kSolveRows, 2) upd_solve_kernel(UpdArgs a, int
   for (int idx = tid; idx < R * R; idx += kSolveRows) Gn[idx] = Gs[idx];
   SOLVE_STAMP(6)
   if (!LAST) {
-    if (n == a.lo_src) slice_lo_columns(a, n, off, R);
+    if (n == a.lo_src) {
+      // nch == 1 (setup_lo_fusion): X holds every solved row unless the pinv
+      // redo used it as scratch
+      if (redo)
+        slice_lo_columns(a, off, R, a.F[n] + off, a.ld);
+      else
+        slice_lo_columns(a, off, R, X, P);
+    }
     return;
   }
   // fast error (als.py:99-115): sum of the Hadamard of all Gramians, folded

@@ -213,6 +213,10 @@ def _run_fused(t: DenseTensor, queue: list[Model], cfg: ConvergenceConfig, r_sta
     lam_off = np.concatenate([[0], np.cumsum(ranks)]).tolist()
     status, err, fit = res.status.tolist(), res.error.tolist(), res.fit.tolist()
     iters, secs = res.iterations.tolist(), res.seconds_active.tolist()
+    if label_per_model:
+        # one instance per call: its wall time is both its seconds_active and
+        # its trace segment, as _run_sequential records them (driver.py:133-144)
+        secs = [wall] * len(secs)
     lam = res.lambdas
     out = []
     try:
@@ -243,7 +247,7 @@ def _run_fused(t: DenseTensor, queue: list[Model], cfg: ConvergenceConfig, r_sta
             for r in out:
                 trace.append(SegmentTrace(
                     label=f"als:{r.id}", flops=_instance_flops(t, r.rank, r.iterations_done),
-                    seconds=wall, meta={"id": r.id, "rank": r.rank,
+                    seconds=r.seconds_active, meta={"id": r.id, "rank": r.rank,
                                         "iterations": r.iterations_done}))
         else:
             for width, n_active, secs in records:

@@ -1,0 +1,31 @@
+"""The Lo-slice fusion of the split update (csrc/update2.cu slice_lo_columns:
+the mode-0 solve writes the Ozaki Lo slices of the next INT8 contraction that
+takes A0 as its Lo operand, which then skips its slicing kernel) forms the
+slices with the slicing kernels' own arithmetic, so a sweep must be bitwise
+identical with and without it (CALS_FUSE_LO=0), for a Y-tree cube and an
+EEM-shaped converging refill sweep."""
+import json
+import os
+import subprocess
+import sys
+
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+
+
+def _run(fuse):
+    env = dict(os.environ, CALS_FUSE_LO=fuse)
+    r = subprocess.run([sys.executable, os.path.join(HERE, "_fuse_worker.py")], env=env,
+                       capture_output=True, text=True, timeout=900)
+    assert r.returncode == 0, r.stderr[-3000:]
+    return json.loads(r.stdout.strip().splitlines()[-1])
+
+
+def test_lo_fusion_bitwise():
+    off, on = _run("0"), _run("1")
+    assert off["eem_iters"] == on["eem_iters"]
+    assert off["cube"] == on["cube"]
+    assert off["eem"] == on["eem"]
