@@ -91,6 +91,20 @@ def run(t: DenseTensor, models: Iterable[Model], cfg: ConvergenceConfig, *,
     return out
 
 
+def _prebuild_results(eng: CalsEngine, queue: list[Model], pool: np.ndarray, shells: list) -> None:
+    """Result Model objects whose factors are (Fortran) views into the result
+    pool ``pool`` -- filled by the device later; scalars set by _run_fused.
+    Runs on a helper thread while the caller sits in the device loop: the
+    initial sleep hands the GIL back so the caller enters the C library
+    (which releases it) before this loop takes it."""
+    time.sleep(0.001)
+    for k, src in enumerate(queue):
+        shells[k] = Model._from_engine(id=src.id, rank=src.rank, factors=eng.unpack(pool, k),
+                                       error=float("nan"), fit=float("nan"), iterations_done=0,
+                                       status=ModelStatus.ACTIVE, seconds_active=0.0,
+                                       meta=dict(src.meta))
+
+
 def _failure_record(src: Model) -> Model:
     """_fit_or_fail's result for an instance whose update raised
     (driver.py:148-160): the starting factors, no iterations, error nan."""
@@ -178,13 +192,20 @@ def _run_fused(t: DenseTensor, queue: list[Model], cfg: ConvergenceConfig, r_sta
         sqnorm = t.device_sqnorm()  # waits for both uploads
         if sqnorm <= 0.0:
             raise _BadNorm()
-        tic = time.perf_counter()
-        eng.run(cfg.tol, cfg.max_iterations, sqnorm)
-        t4 = time.perf_counter()
         # the result pool lands in a fresh page-locked block (torch's caching
         # host allocator -> no cudaHostAlloc per run) that the returned
-        # factors view directly: no host-side copy
+        # factors view directly: no host-side copy.  The result Model objects
+        # (factor views into it) are built by a helper thread while the device
+        # loop runs -- eng.run blocks inside the C library with the GIL
+        # released -- and only get their scalars afterwards.
         pool_t = torch.empty(max(eng.pool_elems, 1), dtype=torch.float64, pin_memory=True)
+        shells: list = [None] * len(queue)
+        builder = threading.Thread(target=_prebuild_results, args=(eng, queue, pool_t.numpy(),
+                                                                   shells), daemon=True)
+        tic = time.perf_counter()
+        builder.start()
+        eng.run(cfg.tol, cfg.max_iterations, sqnorm)
+        t4 = time.perf_counter()
         res = eng.results(with_pool=False)
         # the factor pool comes down while the Model objects are built below
         # (they are views into it); the stream is synchronised before return
@@ -208,7 +229,7 @@ def _run_fused(t: DenseTensor, queue: list[Model], cfg: ConvergenceConfig, r_sta
     if not label_per_model:
         for m in queue:
             m.status = ModelStatus.ACTIVE  # admitted (driver.py:202)
-    pool = pool_t.numpy()
+    builder.join()
     order = np.argsort(res.retire_seq, kind="stable").tolist()
     lam_off = np.concatenate([[0], np.cumsum(ranks)]).tolist()
     status, err, fit = res.status.tolist(), res.error.tolist(), res.fit.tolist()
@@ -230,12 +251,11 @@ def _run_fused(t: DenseTensor, queue: list[Model], cfg: ConvergenceConfig, r_sta
                 rec.seconds_active = secs[k]
                 out.append(rec)
                 continue
-            meta = dict(src.meta)
-            meta["lambdas"] = lam[lam_off[k]:lam_off[k + 1]]
-            out.append(Model._from_engine(id=src.id, rank=src.rank, factors=eng.unpack(pool, k),
-                                          error=err[k], fit=fit[k], iterations_done=iters[k],
-                                          status=STATUS_FROM_CODE[status[k]],
-                                          seconds_active=secs[k], meta=meta))
+            m = shells[k]
+            m.error, m.fit, m.iterations_done = err[k], fit[k], iters[k]
+            m.status, m.seconds_active = STATUS_FROM_CODE[status[k]], secs[k]
+            m.meta["lambdas"] = lam[lam_off[k]:lam_off[k + 1]]
+            out.append(m)
     finally:
         # the factor views are valid once the pool download has landed; only
         # then may another run reuse the engine (and its device pool)
