@@ -19,6 +19,10 @@ import numpy as np
 from . import _native
 from .tensor import hadamard_fold
 
+# largest rank the GPU update kernels take (csrc/update.cuh kMaxRank; the R x R
+# matrix moves from shared memory to global scratch above 128)
+MAX_RANK = 512
+
 
 @dataclass
 class ConvergenceConfig:
@@ -74,8 +78,8 @@ def update_factor(m: np.ndarray, h: np.ndarray) -> np.ndarray:
     if m.ndim != 2 or m.shape[1] != h.shape[0]:
         raise ValueError(f"m has shape {m.shape}, expected (*, {h.shape[0]})")
     rows, r = m.shape
-    if r > 128:
-        raise ValueError("update_factor supports rank <= 128 on the GPU")
+    if r > MAX_RANK:
+        raise ValueError(f"update_factor supports rank <= {MAX_RANK} on the GPU")
     lib = _native.load()
     dev = torch.device("cuda", torch.cuda.current_device())
     md = torch.from_numpy(np.ascontiguousarray(m)).to(dev)

@@ -34,7 +34,10 @@ namespace cals {
 
 // ------------------------------------------------------------------ update --
 // RB > 0: fast path (every rank <= RB, rows in registers, chunked Gram);
-// RB == 0: generic path for ranks up to 128.  Same reference semantics.
+// RB == 0: generic path (block Cholesky / row solves / Jacobi pinv) for ranks
+// up to kMaxRank; up to kSmemRankMax the R x R matrix lives in shared memory,
+// above it in the block's global scratch slice (L2-resident).  Same
+// reference semantics.
 #ifdef CALS_UPD_PROFILE
 __device__ long long g_upd_prof[3][4096][13];
 #define UPD_STAMP(i) \
@@ -68,11 +71,12 @@ __global__ void __launch_bounds__(kUpdThreads, 2) engine_update_kernel(
   EngState* const st = &sst;
   const int N = st->order;
   const int Rmax = st->max_rank;
-  double* H = dsm;                // Rmax^2
-  double* X = H + Rmax * Rmax;    // generic: Rmax * nthr; fast: kUpdThreads * (RB + 1)
-  double* V = st->scratch + (long long)blockIdx.x * (2 * Rmax * Rmax + Rmax);
+  const bool big = Rmax > kSmemRankMax;
+  double* V = st->scratch + (long long)blockIdx.x * upd_scratch_doubles(Rmax);
   double* Hsave = V + Rmax * Rmax;
   double* lam = Hsave + Rmax * Rmax;
+  double* H = big ? lam + Rmax : dsm;     // Rmax^2
+  double* X = big ? dsm : H + Rmax * Rmax;  // generic: Rmax * nthr; fast: kUpdThreads * (RB + 1)
   const int rows = (int)st->dims[n];
   const long long ld = st->ld;
   const int n_active = st->n_active;
@@ -613,8 +617,10 @@ __global__ void __launch_bounds__(kUpdThreads) standalone_update_kernel(
     double* scratch, int nthr, int* status) {
   extern __shared__ __align__(16) double dsm[];
   __shared__ int flag;
-  double* H = dsm;
-  double* X = H + R * R;
+  // scratch: V (R^2), Hsave (R^2), lam (R), and H (R^2) above kSmemRankMax
+  const bool big = R > kSmemRankMax;
+  double* H = big ? scratch + 2 * R * R + R : dsm;
+  double* X = big ? dsm : H + R * R;
   for (int idx = threadIdx.x; idx < R * R; idx += blockDim.x) H[idx] = Hin[idx];
   __syncthreads();
   const bool ok = block_update(H, scratch + R * R, scratch, scratch + 2 * R * R, X, nthr, R, Mb,
@@ -843,7 +849,8 @@ static int engine_create(Tensor* t, int capacity, int n_models, const int* ranks
     rmax = std::max(rmax, ranks[k]);
     rsum += ranks[k];
   }
-  CALS_CHECK(rmax <= 128, kErrUnsupported, "ranks above 128 are not supported by the update kernel");
+  CALS_CHECK(rmax <= kMaxRank, kErrUnsupported,
+             "ranks above " + std::to_string(kMaxRank) + " are not supported by the update kernel");
   e->max_rank = rmax;
   e->max_slots = std::max(1, std::min<int>(n_models, capacity));
   e->ld = align_up(capacity, 8);
@@ -873,7 +880,7 @@ static int engine_create(Tensor* t, int capacity, int n_models, const int* ranks
   e->upd_grid = std::max(1, std::min(e->max_slots, sms * 4));
   e->upd_nthr = pick_nthr(rmax);
   e->upd_kernel = update_kernel_for(rmax, &e->upd_rb);
-  e->upd_smem = size_t(rmax) * rmax * 8 +
+  e->upd_smem = (rmax > kSmemRankMax ? 0 : size_t(rmax) * rmax * 8) +
                 std::max(size_t(rmax) * e->upd_nthr, size_t(kUpdThreads) * (e->upd_rb + 1)) * 8;
   e->move_smem = size_t(e->ld) * 8;
   long long rows_total = 0, maxI = 1;
@@ -924,8 +931,7 @@ static int engine_create(Tensor* t, int capacity, int n_models, const int* ranks
     fbytes_total += t->dims[n] * e->ld * 8;
   }
   items.push_back({(void**)&h.Mout, size_t(maxI) * e->ld * 8});
-  items.push_back({(void**)&h.scratch,
-                   size_t(e->upd_grid) * (2 * rmax * rmax + rmax) * 8});
+  items.push_back({(void**)&h.scratch, size_t(e->upd_grid) * upd_scratch_doubles(rmax) * 8});
   items.push_back({(void**)&h.tr_width, size_t(e->trace_cap) * 4});
   items.push_back({(void**)&h.tr_active, size_t(e->trace_cap) * 4});
   items.push_back({(void**)&h.tr_time, size_t(e->trace_cap) * 8});
@@ -1598,10 +1604,12 @@ int cals_mttkrp_variants(int* count) {
 
 int cals_update_factor(int rows, int rank, const double* m, int64_t ldm, const double* h,
                        double* a, int64_t lda, double* scratch, int* status, void* stream) {
-  CALS_CHECK(rows >= 0 && rank >= 1 && rank <= 128, kErrInvalid, "rank must be in [1, 128]");
+  CALS_CHECK(rows >= 0 && rank >= 1 && rank <= kMaxRank, kErrInvalid,
+             "rank must be in [1, " + std::to_string(kMaxRank) + "]");
   CALS_CHECK(m && h && a && scratch && status, kErrInvalid, "null argument");
   const int nthr = pick_nthr(rank);
-  const size_t smem = size_t(rank) * rank * 8 + size_t(rank) * nthr * 8;
+  const size_t smem =
+      (rank > kSmemRankMax ? 0 : size_t(rank) * rank * 8) + size_t(rank) * nthr * 8;
   CALS_CUDA_TRY(raise_smem_limit((const void*)standalone_update_kernel, smem));
   standalone_update_kernel<<<1, kUpdThreads, smem, (cudaStream_t)stream>>>(
       m, ldm, rows, rank, h, a, lda, scratch, nthr, status);

@@ -19,6 +19,16 @@
 namespace cals {
 
 constexpr int kUpdThreads = 256;
+// Generic update path limits: the R x R matrix of the block routines below
+// lives in shared memory up to kSmemRankMax, in global scratch above it;
+// the row tile (R x >= 32 threads' rows) bounds the rank at kMaxRank.
+constexpr int kSmemRankMax = 128;
+constexpr int kMaxRank = 512;
+// per-block global scratch of the engine's update kernel (doubles): V, Hsave
+// (R^2 each), lam (R), and H (R^2) above kSmemRankMax
+__host__ __device__ constexpr long long upd_scratch_doubles(int R) {
+  return 2LL * R * R + R + (R > kSmemRankMax ? (long long)R * R : 0LL);
+}
 
 // Deterministic block sum (blockDim.x a multiple of 32; `red` has >= 32
 // doubles): an xor butterfly inside each warp (partners add the same two

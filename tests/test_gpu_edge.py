@@ -48,6 +48,27 @@ def test_generic_update_path_ranks_above_32(cals):
     _vs_oracle(cals, (40, 36, 34), [33, 40], 1, 0.0, 4, 80, fac_tol=1e-8)
 
 
+def test_generic_update_path_ranks_above_128(cals):
+    """R > 128: the generic update keeps its R x R matrix in global scratch
+    (csrc/update.cuh kSmemRankMax); the reference has no rank limit."""
+    _vs_oracle(cals, (170, 165, 160), [130, 150], 1, 0.0, 3, 280, fac_tol=1e-8)
+
+
+def test_update_factor_rank_200(cals):
+    """The operator API (als.py:74-96) at rank 200 against scipy's cho_solve."""
+    from scipy.linalg import cho_factor, cho_solve
+
+    rng = np.random.default_rng(11)
+    a = rng.random((260, 200))
+    h = a.T @ a + np.eye(200)
+    m = rng.standard_normal((90, 200))
+    want = cho_solve(cho_factor(h, lower=False), m.T).T
+    got = cals.update_factor(m, h)
+    assert np.linalg.norm(got - want) / np.linalg.norm(want) <= 1e-10
+    with pytest.raises(ValueError):
+        cals.update_factor(np.ones((2, 513)), np.eye(513))
+
+
 @pytest.mark.parametrize("ranks", [[1, 8], [9, 16], [17, 24], [25, 32]])
 def test_update_rank_buckets(cals, ranks):
     """The update kernel is instantiated per rank bucket (largest rank of the
