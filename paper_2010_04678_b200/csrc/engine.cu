@@ -554,6 +554,7 @@ __global__ void __launch_bounds__(kPlanThreads, 1) engine_plan_kernel(EngState* 
     }
     st->plans_done = rec + 1;
     *st->changed = 0;
+    *st->lo_stale = 1;  // columns may have moved: carried Lo slices are stale
     if (new_n == 0 && head >= st->n_models) {
       st->done = 1;
       st->host_done[1] = rec + 1;  // plan count, read by the host without a copy
@@ -700,6 +701,7 @@ struct Engine {
   bool split = false;
   UpdArgs ua{};
   int lo_target = -1;  // mode whose contraction takes its Lo slices from solve(0)
+  bool lo_carry = false;  // mode 0's Lo slices carried over from the previous iteration
   PrepKernel prep_kernel = nullptr;
   SolveKernel solve_kernel = nullptr, solve_last_kernel = nullptr;
   size_t solve_smem = 0;
@@ -904,6 +906,7 @@ static int engine_create(Tensor* t, int capacity, int n_models, const int* ranks
   items.push_back({(void**)&h.slot_off, size_t(ms) * 4});
   items.push_back({(void**)&h.slot_info, size_t(ms) * 16});
   items.push_back({(void**)&h.changed, 4});
+  items.push_back({(void**)&h.lo_stale, 4});
   items.push_back({(void**)&h.mv_kind, size_t(mv) * 4});
   items.push_back({(void**)&h.mv_model, size_t(mv) * 4});
   items.push_back({(void**)&h.mv_src, size_t(mv) * 4});
@@ -981,7 +984,9 @@ static int engine_create(Tensor* t, int capacity, int n_models, const int* ranks
   }
   ua.ld = e->ld;
   ua.order = N;
-  ua.lo_src = -1;
+  ua.lo[0].src = -1;
+  ua.lo[1].src = -1;
+  ua.lo_stale = h.lo_stale;
   if (e->split) {
     split_kernels_for(e->upd_rb, &e->prep_kernel, &e->solve_kernel, &e->solve_last_kernel,
                       &e->solve_smem);
@@ -1036,7 +1041,10 @@ static int engine_create(Tensor* t, int capacity, int n_models, const int* ranks
 // iteration count, failure / fresh flags 0, retirement order -1, f_prev =
 // -inf, error = +inf, fit = -inf.
 __global__ void engine_reset_kernel(const EngState h, int nm) {
-  if (blockIdx.x == 0 && threadIdx.x == 0) *h.changed = 0;
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    *h.changed = 0;
+    *h.lo_stale = 1;
+  }
   for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < nm; k += gridDim.x * blockDim.x) {
     h.status[k] = 0;
     h.iters[k] = 0;
@@ -1133,7 +1141,7 @@ static int enqueue_mode_mttkrp(Engine* e, int n, cudaStream_t stream) {
       // the partial Y[i + I0p j] kept for mode 1
       rc = launch_contraction(t, e->tree_plan, 100, F[2], t.dims[2], ld, F[1], ld, 0, wptr, cap,
                               Mo, ld, e->d_ws, e->tree_variant, stream, e->d_partial, ld, t.i0p,
-                              oz_ws, oz_bytes);
+                              oz_ws, oz_bytes, false, e->lo_carry ? e->h_st.lo_stale : nullptr);
     } else if (e->tree == kTreeY && n == 1) {
       // M1 = Y x_i A0(new): A2 unchanged since Y was formed
       rc = launch_partial_ttv(e->d_partial, ld, t.i0p, t.dims[1], 0, t.dims[0], F[0], ld, 0,
@@ -1149,7 +1157,8 @@ static int enqueue_mode_mttkrp(Engine* e, int n, cudaStream_t stream) {
                               wptr, cap, t.dims[2], Mo, ld, sms, stream);
     } else {
       rc = launch_mttkrp(t, n, fs, 0, wptr, cap, Mo, ld, e->d_ws, e->ws_bytes, e->variants[n],
-                         stream, n == e->lo_target);
+                         stream, n == e->lo_target,
+                         (n == 0 && e->lo_carry) ? e->h_st.lo_stale : nullptr);
     }
     if (rc) return rc;
   }
@@ -1360,7 +1369,7 @@ static int engine_capture(Engine* e, cudaStream_t stream) {
 
 // Run every queued model to retirement.  `pool` must already hold the
 // starting factors (per model, per mode, row-major I_n x R_k).
-// Lo-slice fusion (UpdArgs::lo_src): when the first contraction after mode 0
+// Lo-slice fusion (UpdArgs::lo): when the first contraction after mode 0
 // takes F[0] (just solved) as its Lo operand and runs on the INT8 path, the
 // mode-0 solve kernel writes that contraction's Lo slices, exponents and
 // unit counter, and the contraction skips its slicing kernel (one launch and
@@ -1370,37 +1379,69 @@ static int engine_capture(Engine* e, cudaStream_t stream) {
 // disables it.
 static void setup_lo_fusion(Engine* e) {
   e->lo_target = -1;
-  e->ua.lo_src = -1;
+  e->lo_carry = false;
+  e->ua.lo[0].src = -1;
+  e->ua.lo[1].src = -1;
+  e->ua.lo_stale = e->h_st.lo_stale;
   const char* env = getenv("CALS_FUSE_LO");
   if (env && atoi(env) == 0) return;
-  if (!e->split || e->h_st.nonneg || e->h_st.ls_enabled || e->order != 3 || e->nch[0] != 1)
-    return;
+  if (!e->split || e->h_st.nonneg || e->h_st.ls_enabled || e->order != 3) return;
   Tensor& t = *e->t;
-  for (int n = 1; n < e->order; ++n) {
-    if ((e->tree == kTreeY && n == 1) || (e->tree == kTreeZ && n == 2)) continue;  // TTV
-    const ModePlan* p;
-    void* ws;
-    int key = n;
-    if (e->tree == kTreeZ && n == 1) {  // Z = X x_1 A0(new): Lo = F[0]
-      p = &e->tree_plan;
-      ws = reinterpret_cast<char*>(e->d_ws) + tree_ws_offset(e->tree_plan, e->ld);
-    } else {
-      p = &t.plans[n];
-      if (!p->lo_direct() || p->lo_modes[0] != 0) return;
-      ws = mttkrp_oz_ws(t, n, e->ld, e->d_ws, e->ws_bytes);
+  auto fill = [&](UpdArgs::LoTarget& tg, const ModePlan& p, int lo_mode, void* ws, int src) {
+    const OzLoLayout l = ozaki_lo_layout(p, t.dims[lo_mode], e->capacity, ws);
+    tg.ls = l.ls;
+    tg.cex = l.cex;
+    tg.queue = l.queue;
+    tg.stride = l.slice_stride;
+    tg.Kp = l.Kp;
+    tg.Dp = l.Dp;
+    tg.src = src;
+  };
+  // target 0: the first contraction after mode 0 that takes F[0] as Lo
+  if (e->nch[0] == 1) {
+    for (int n = 1; n < e->order; ++n) {
+      if ((e->tree == kTreeY && n == 1) || (e->tree == kTreeZ && n == 2)) continue;  // TTV
+      const ModePlan* p;
+      void* ws;
+      if (e->tree == kTreeZ && n == 1) {  // Z = X x_1 A0(new): Lo = F[0]
+        p = &e->tree_plan;
+        ws = reinterpret_cast<char*>(e->d_ws) + tree_ws_offset(e->tree_plan, e->ld);
+      } else {
+        p = &t.plans[n];
+        if (!p->lo_direct() || p->lo_modes[0] != 0) break;
+        ws = mttkrp_oz_ws(t, n, e->ld, e->d_ws, e->ws_bytes);
+      }
+      if (ws && ozaki_ready(t, *p, n)) {
+        fill(e->ua.lo[0], *p, 0, ws, 0);
+        e->lo_target = n;
+      }
+      break;
     }
-    if (!ws || !ozaki_ready(t, *p, key)) return;
-    const OzLoLayout l = ozaki_lo_layout(*p, t.dims[0], e->capacity, ws);
-    UpdArgs& ua = e->ua;
-    ua.lo_ls = l.ls;
-    ua.lo_cex = l.cex;
-    ua.lo_queue = l.queue;
-    ua.lo_stride = l.slice_stride;
-    ua.lo_Kp = l.Kp;
-    ua.lo_Dp = l.Dp;
-    ua.lo_src = 0;
-    e->lo_target = n;
-    return;
+  }
+  // target 1 (carry): the next iteration's mode-0 contraction, written by the
+  // solve of its Lo mode when nothing between that solve and mode 0 contracts
+  // through the shared workspace (tree schedules: the modes in between are a
+  // TTV); its slicing kernel still runs whenever the plan moved columns
+  {
+    const ModePlan* p = nullptr;
+    void* ws = nullptr;
+    int key = 0, src = -1;
+    if (e->tree == kTreeY) {  // mode 0: Y-tree contraction, Lo = F[2]
+      p = &e->tree_plan;
+      key = 100;
+      src = 2;
+      ws = reinterpret_cast<char*>(e->d_ws) + tree_ws_offset(e->tree_plan, e->ld);
+    } else if (e->tree == kTreeZ && t.plans[0].lo_direct()) {  // mode 0 plain, mode 2 a TTV
+      p = &t.plans[0];
+      key = 0;
+      src = t.plans[0].lo_modes[0];
+      ws = mttkrp_oz_ws(t, 0, e->ld, e->d_ws, e->ws_bytes);
+    }
+    if (p && src > 0 && src < e->order && e->nch[src] == 1 && ws && ozaki_ready(t, *p, key)) {
+      fill(e->ua.lo[1], *p, src, ws, src);
+      e->ua.lo[1].queue = nullptr;  // zeroed by the (always launched) slicing kernel
+      e->lo_carry = true;
+    }
   }
 }
 
@@ -1884,7 +1925,9 @@ int cals_engine_begin(cals_engine* e, double tol, int max_iterations, double sqn
   if (rc) return rc;
   // the step-wise driver reduces partial MTTKRPs between the calls: no fusion
   g->lo_target = -1;
-  g->ua.lo_src = -1;
+  g->lo_carry = false;
+  g->ua.lo[0].src = -1;
+  g->ua.lo[1].src = -1;
   return enqueue_plan(g, s);  // initial admission
 }
 

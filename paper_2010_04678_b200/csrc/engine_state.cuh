@@ -33,6 +33,10 @@ struct EngState {
   // zero -> the next plan is a no-op (no retirement frees width, so no
   // admission is possible either)
   int* changed;
+  // Lo-slice carry (UpdArgs::lo[1]): 1 when the column layout changed since
+  // the solve kernel last wrote the next mode-0 contraction's Lo slices (set
+  // by a plan that did work and at reset), 0 once that solve has written them
+  int* lo_stale;
   // move plan
   int* mv_kind;
   int* mv_model;

@@ -120,7 +120,7 @@ struct FactorSet {
 int launch_mttkrp(Tensor& t, int mode, const FactorSet& f, int width, const int* width_ptr,
                   long long cap, double* out, long long ldo, double* workspace,
                   size_t workspace_bytes, int variant, cudaStream_t stream,
-                  bool lo_sliced = false);
+                  bool lo_sliced = false, const int* lo_stale = nullptr);
 // The Ozaki workspace launch_mttkrp carves for `mode` out of `workspace`
 // (nullptr when the mode does not run on the INT8 path or it does not fit).
 void* mttkrp_oz_ws(Tensor& t, int mode, long long ld, void* workspace, size_t workspace_bytes);
@@ -136,7 +136,8 @@ int launch_contraction(Tensor& t, const ModePlan& p, int map_key, const double* 
                        int width, const int* width_ptr, long long cap, double* out, long long ldo,
                        double* part, int variant, cudaStream_t stream, double* side = nullptr,
                        long long side_ld = 0, long long side_qstride = 0, void* oz_ws = nullptr,
-                       size_t oz_ws_bytes = 0, bool lo_sliced = false);
+                       size_t oz_ws_bytes = 0, bool lo_sliced = false,
+                       const int* lo_stale = nullptr);
 
 // Ozaki-sliced INT8 tensor-core contraction (ozaki.cu) ------------------------
 bool ozaki_enabled();                       // CALS_MTTKRP=dmma disables it
@@ -159,7 +160,8 @@ bool ozaki_ready(Tensor& t, const ModePlan& p, int key);
 // ls[7][cap_pad][Kp] (column c of Lo as a p-contiguous row), cex[c], and the
 // work-unit counter.  A producer that writes them itself (the split update's
 // solve kernel, update2.cu) lets the contraction skip its slicing kernel
-// (lo_sliced = true).
+// (lo_sliced = true), or run it only while *lo_stale != 0 (lo_stale: device
+// flag, nullptr = always slice).
 struct OzLoLayout {
   uint8_t* ls = nullptr;
   int* cex = nullptr;
@@ -174,7 +176,8 @@ int launch_contraction_ozaki(Tensor& t, const ModePlan& p, int key, const double
                              int width, const int* width_ptr, long long cap, double* out,
                              long long ldo, double* part, void* oz_ws, size_t oz_ws_bytes,
                              cudaStream_t stream, double* side, long long side_ld,
-                             long long side_qstride, bool lo_sliced = false);
+                             long long side_qstride, bool lo_sliced = false,
+                             const int* lo_stale = nullptr);
 
 // out[row][c] = sum over the reduced index of P[a + Da*b][c] * F[idx][c]
 // (reduce_b: rows a < rows_out, sum b < Db with F[b]; else rows b, sum a < La

@@ -137,13 +137,14 @@ __global__ void oz_slice_rows_kernel(const double* __restrict__ x, long long sm,
 __global__ void oz_slice_cols_kernel(const double* __restrict__ lo, long long ld, int Dp, int Kp,
                                      const int* width_ptr, int width, long long cap_pad,
                                      uint8_t* __restrict__ ls, int* __restrict__ cex,
-                                     int* __restrict__ queue) {
+                                     int* __restrict__ queue, const int* __restrict__ stale) {
   __shared__ double tile[32][33];
   __shared__ double red[8][33];
   __shared__ int ex[32];
   griddep_wait();  // launched with PDL (launch_dep): predecessors complete
   // the contraction kernel that follows claims its work units from *queue
   if (blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0) *queue = 0;
+  if (stale && *stale == 0) return;  // the solve kernel already wrote these slices
   const int W = width_ptr ? *width_ptr : width;
   const int c0 = blockIdx.x * 32, p0 = blockIdx.y * 32;
   if (c0 >= W) return;
@@ -202,12 +203,14 @@ __global__ void oz_slice_cols_kernel(const double* __restrict__ lo, long long ld
 constexpr int kColsAllMaxKp = 256;
 __global__ void __launch_bounds__(256) oz_slice_cols_all_kernel(
     const double* __restrict__ lo, long long ld, int Dp, int Kp, const int* width_ptr, int width,
-    long long cap_pad, uint8_t* __restrict__ ls, int* __restrict__ cex, int* __restrict__ queue) {
+    long long cap_pad, uint8_t* __restrict__ ls, int* __restrict__ cex, int* __restrict__ queue,
+    const int* __restrict__ stale) {
   extern __shared__ double ctile[];  // [Kp][33]
   __shared__ double red[8][33];
   __shared__ int ex[32];
   griddep_wait();  // launched with PDL (launch_dep): predecessors complete
   if (blockIdx.x == 0 && threadIdx.x == 0) *queue = 0;
+  if (stale && *stale == 0) return;  // the solve kernel already wrote these slices
   const int W = width_ptr ? *width_ptr : width;
   const int c0 = blockIdx.x * 32;
   if (c0 >= W) return;
@@ -504,7 +507,7 @@ int launch_contraction_ozaki(Tensor& t, const ModePlan& p, int key, const double
                              int width, const int* width_ptr, long long cap, double* out,
                              long long ldo, double* part, void* oz_ws, size_t oz_ws_bytes,
                              cudaStream_t stream, double* side, long long side_ld,
-                             long long side_qstride, bool lo_sliced) {
+                             long long side_qstride, bool lo_sliced, const int* lo_stale) {
   OzSlices o;
   {
     std::lock_guard<std::mutex> lk(t.mu);
@@ -541,12 +544,13 @@ int launch_contraction_ozaki(Tensor& t, const ModePlan& p, int key, const double
     CALS_CUDA_TRY(attr);
     CALS_CUDA_TRY(launch_dep(oz_slice_cols_all_kernel, dim3((unsigned)((cap + 31) / 32)), dim3(256),
                              smem, stream, lo, lo_ld, (int)std::min<long long>(lrows, p.Dp),
-                             (int)o.Kp, width_ptr, width, (long long)cap_pad, ls, cex, queue));
+                             (int)o.Kp, width_ptr, width, (long long)cap_pad, ls, cex, queue,
+                             lo_stale));
   } else {
     CALS_CUDA_TRY(launch_dep(oz_slice_cols_kernel,
                              dim3((unsigned)((cap + 31) / 32), (unsigned)(o.Kp / 32)), dim3(256), 0,
                              stream, lo, lo_ld, (int)std::min<long long>(lrows, p.Dp), (int)o.Kp,
-                             width_ptr, width, (long long)cap_pad, ls, cex, queue));
+                             width_ptr, width, (long long)cap_pad, ls, cex, queue, lo_stale));
   }
   CALS_CUDA_TRY(cudaGetLastError());
 

@@ -336,12 +336,12 @@ __device__ __forceinline__ void tile_gram_tc(const double* __restrict__ X, int P
 // zeros for p in [Dp, Kp).  A / ld: the factor block -- the solved rows still
 // in shared memory, or (failure / pinv-redo paths) F[n] in global memory
 // (this CTA's own stores, visible after the barrier that precedes the call).
-__device__ __noinline__ void slice_lo_columns(const UpdArgs& a, int off, int R,
+__device__ __noinline__ void slice_lo_columns(const UpdArgs::LoTarget& tg, int off, int R,
                                               const double* __restrict__ A, long long ld) {
   __shared__ int ex_s[32];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int Dp = a.lo_Dp, Kp = a.lo_Kp;
-  if (blockIdx.x == 0 && tid == 0) *a.lo_queue = 0;  // the contraction's unit counter
+  const int Dp = tg.Dp, Kp = tg.Kp;
+  if (tg.queue && blockIdx.x == 0 && tid == 0) *tg.queue = 0;  // the contraction's unit counter
   for (int c = warp; c < R; c += kSolveRows / 32) {
     double mx = 0.0;
 #pragma unroll 4
@@ -351,7 +351,7 @@ __device__ __noinline__ void slice_lo_columns(const UpdArgs& a, int off, int R,
     if (lane == 0) {
       const int e = oz::scale_exp_checked(mx);
       ex_s[c] = e;
-      a.lo_cex[off + c] = e;
+      tg.cex[off + c] = e;
     }
   }
   __syncthreads();
@@ -370,11 +370,22 @@ __device__ __noinline__ void slice_lo_columns(const UpdArgs& a, int off, int R,
 #pragma unroll
       for (int s = 0; s < oz::kSlices; ++s) w[s] |= uint32_t(sl[s]) << (8 * u);
     }
-    uint8_t* dst = a.lo_ls + size_t(off + c) * Kp + p0;
+    uint8_t* dst = tg.ls + size_t(off + c) * Kp + p0;
 #pragma unroll
     for (int s = 0; s < oz::kSlices; ++s)
-      *reinterpret_cast<uint32_t*>(dst + size_t(s) * a.lo_stride) = w[s];
+      *reinterpret_cast<uint32_t*>(dst + size_t(s) * tg.stride) = w[s];
   }
+}
+
+// Every fusion target fed by the solve of mode n (UpdArgs::lo); block-uniform.
+__device__ __forceinline__ void slice_lo_targets(const UpdArgs& a, int n, int off, int R,
+                                                 const double* A, long long ld) {
+#pragma unroll
+  for (int t = 0; t < 2; ++t)
+    if (a.lo[t].src == n) {
+      slice_lo_columns(a.lo[t], off, R, A, ld);
+      if (t == 1 && blockIdx.x == 0 && threadIdx.x == 0) *a.lo_stale = 0;
+    }
 }
 
 // Shared-memory layout of upd_solve_kernel<RB> (doubles)
@@ -424,9 +435,9 @@ __global__ void __launch_bounds__(kSolveRows, 2) upd_solve_kernel(UpdArgs a, int
   SOLVE_STAMP(1)
   if (pf == kPrepFailed) {  // failed earlier in this iteration (driver.py:218-219)
     if (LAST && chunk == 0 && tid == 0) finish_model(a, k, 0.0, 0.0, false);
-    if (!LAST && n == a.lo_src) {  // the factor stays: its slices still feed the next contraction
-      griddep_wait();
-      slice_lo_columns(a, off, R, a.F[n] + off, a.ld);
+    if (a.lo[0].src == n || a.lo[1].src == n) {  // the factor stays: its slices still feed
+      griddep_wait();                                 // the later contraction
+      slice_lo_targets(a, n, off, R, a.F[n] + off, a.ld);
     }
     return;
   }
@@ -503,7 +514,7 @@ __global__ void __launch_bounds__(kSolveRows, 2) upd_solve_kernel(UpdArgs a, int
       a.failed[k] = 1;
       if (LAST) finish_model(a, k, 0.0, 0.0, false);
     }
-    if (!LAST && n == a.lo_src) slice_lo_columns(a, off, R, a.F[n] + off, a.ld);
+    slice_lo_targets(a, n, off, R, a.F[n] + off, a.ld);
     return;
   }
   int sbad = 0;
@@ -614,17 +625,13 @@ __global__ void __launch_bounds__(kSolveRows, 2) upd_solve_kernel(UpdArgs a, int
   __syncthreads();  // Gs final
   for (int idx = tid; idx < R * R; idx += kSolveRows) Gn[idx] = Gs[idx];
   SOLVE_STAMP(6)
-  if (!LAST) {
-    if (n == a.lo_src) {
-      // nch == 1 (setup_lo_fusion): X holds every solved row unless the pinv
-      // redo used it as scratch
-      if (redo)
-        slice_lo_columns(a, off, R, a.F[n] + off, a.ld);
-      else
-        slice_lo_columns(a, off, R, X, P);
-    }
-    return;
-  }
+  // nch == 1 for a fusion source (setup_lo_fusion): X holds every solved row
+  // unless the pinv redo used it as scratch
+  if (redo)
+    slice_lo_targets(a, n, off, R, a.F[n] + off, a.ld);
+  else
+    slice_lo_targets(a, n, off, R, X, P);
+  if (!LAST) return;
   // fast error (als.py:99-115): sum of the Hadamard of all Gramians, folded
   // ascending -- (G_0 o .. o G_{N-2}) from prep, then o G_{N-1}
   double mpart = 0.0;

@@ -59,17 +59,24 @@ struct UpdArgs {
   long long dims[kMaxOrder];
   long long ld;
   int order;
-  // Lo-slice fusion: the solve of mode lo_src (-1: none) also writes the
-  // Ozaki Lo slices of its factor columns for the next INT8 contraction that
-  // takes F[lo_src] as its Lo operand (the oz_slice_cols* arithmetic; that
-  // contraction then skips its slicing kernel).  OzLoLayout in internal.h.
-  uint8_t* lo_ls;
-  int* lo_cex;
-  int* lo_queue;
-  long long lo_stride;  // cap_pad * Kp
-  int lo_Kp;
-  int lo_Dp;
-  int lo_src;
+  // Lo-slice fusion: the solve of mode lo[t].src (-1: none) also writes the
+  // Ozaki Lo slices of its factor columns for a later INT8 contraction that
+  // takes F[src] as its Lo operand (the oz_slice_cols* arithmetic).  Target 0
+  // is consumed in the same driver iteration (that contraction skips its
+  // slicing kernel); target 1 by the next iteration's mode-0 contraction,
+  // whose slicing kernel only runs when the plan changed the column layout
+  // in between (*lo_stale, set by the plan kernel, cleared here).
+  // OzLoLayout in internal.h.
+  struct LoTarget {
+    uint8_t* ls;
+    int* cex;
+    int* queue;           // the contraction's unit counter (target 0 zeroes it)
+    long long stride;     // cap_pad * Kp
+    int Kp;
+    int Dp;
+    int src;
+  } lo[2];
+  int* lo_stale;
 };
 
 // Shared memory of upd_solve_kernel<RB> (SolveSmem in update2.cu):

@@ -1,9 +1,10 @@
 """The Lo-slice fusion of the split update (csrc/update2.cu slice_lo_columns:
-the mode-0 solve writes the Ozaki Lo slices of the next INT8 contraction that
-takes A0 as its Lo operand, which then skips its slicing kernel) forms the
-slices with the slicing kernels' own arithmetic, so a sweep must be bitwise
-identical with and without it (CALS_FUSE_LO=0), for a Y-tree cube and an
-EEM-shaped converging refill sweep."""
+solves write the Ozaki Lo slices of a later INT8 contraction with the slicing
+kernels' arithmetic -- in the same iteration, whose contraction then skips
+its slicing kernel, and carried into the next iteration's mode-0
+contraction, sliced again only after the plan moved columns) must leave a
+sweep bitwise identical (CALS_FUSE_LO=0 turns it off): a Y-tree cube and an
+EEM-shaped converging refill sweep whose plans move columns."""
 import json
 import os
 import subprocess
