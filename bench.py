@@ -373,11 +373,12 @@ def main_gpu(args) -> None:
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")
     sq = t.sqnorm
 
-    iters_run = []
+    iters_run, launches_run = [], []
 
     def step():
         eng.load_pool(pool_dev)
         iters_run.append(eng.run(wl["tol"], wl["iters"], sq))
+        launches_run.append(eng.last_launches())
 
     for _ in range(args.warmup):
         step()
@@ -407,15 +408,10 @@ def main_gpu(args) -> None:
         dist.all_reduce(tmax, op=dist.ReduceOp.MAX)
     ms_max = float(tmax.item())
     value = total_models / (ms_max * 1e-3)
-    # launches per step (matches the ncu launch list of tools/ncu_engine.py):
-    # per driver iteration, order 3 with the dimension tree: two tensor-core
-    # contractions (+ split reduce, + the per-call Lo slicing on the INT8
-    # path), one partial TTV, three updates, plan + move; per run the state
-    # reset kernel and the initial plan + move
-    k2, o2 = C.c_int32(), C.c_double()
-    _native.call("cals_mttkrp_kernel_info", dev_t.handle, 2, r_star, C.byref(k2), C.byref(o2))
-    per_contraction = 2 + (1 if k2.value == 1 else 0)
-    gpu_launches = int(round(np.mean(iters_run))) * (2 * per_contraction + 1 + 3 + 2) + 3
+    # our kernels launched inside the timed region, counted by the library for
+    # every run (kernel nodes of the captured iteration graph x graph
+    # launches + reset / initial plan / move; cals_engine_last_launches)
+    gpu_launches = int(sum(launches_run[-args.steps:]))
 
     # ---- e2e through the public API with host buffers
     from paper_2010_04678_b200.driver import LAST_RUN_PROFILE
@@ -526,6 +522,7 @@ def main_gpu(args) -> None:
     cfg = _config(name, world)
     details = {"models_this_gpu": n_models, "r_star_this_gpu": r_star,
                "driver_iterations_per_step": it_mean,
+               "gpu_launches_per_step": gpu_launches / max(1, args.steps),
                "mttkrp_kernels": {f"mode{n}": ("int8-ozaki" if k == 1 else "fp64-dmma")
                                   for n, k in enumerate(kinds)},
                "tensor_slices": "the INT8 path's tensor slices (a derived format of the "

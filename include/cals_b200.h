@@ -121,6 +121,11 @@ int cals_engine_results(cals_engine* e, double* pool, int32_t* status, int32_t* 
  * caller synchronises the stream before reading it (run() builds the
  * returned Model objects while the copy is in flight). */
 int cals_engine_pool_download(cals_engine* e, double* host_pool, void* stream);
+/* Kernel launches of the last cals_engine_run (graph path): kernel nodes of
+ * the captured driver-iteration graph x graph launches, plus the reset,
+ * initial plan and move kernels.  Measurement only -- the reference has no
+ * counterpart (its driver loop, driver.py:185-285, is host code). */
+int cals_engine_last_launches(cals_engine* e, long long* launches);
 /* One record per driver iteration (driver.py:278-284 SegmentTrace meta). */
 int cals_engine_trace(cals_engine* e, int32_t* widths, int32_t* n_active, double* seconds,
                       int capacity, int* count);

@@ -53,6 +53,7 @@ SIGNATURES = {
                                       C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
                                       C.c_void_p]),
     "cals_engine_pool_download": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p]),
+    "cals_engine_last_launches": (C.c_int, [C.c_void_p, C.c_void_p]),
     "cals_engine_trace": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int,
                                     c_int_p]),
     "cals_engine_variant": (C.c_int, [C.c_void_p, C.c_int, c_int_p, c_int_p, c_int_p, c_int_p]),

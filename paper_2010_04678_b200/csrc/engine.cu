@@ -715,6 +715,10 @@ struct Engine {
   cudaStream_t cap_stream = nullptr;
   int trace_cap = 0;
   int last_iterations = 0;
+  // kernel launches of the last engine_run: kernel nodes of the captured
+  // iteration graph x graph launches + the kernels launched directly
+  int graph_kernels = 0;
+  long long last_launches = 0;
 };
 
 static size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
@@ -1367,6 +1371,21 @@ static int engine_capture(Engine* e, cudaStream_t stream) {
   return kOk;
 }
 
+// Kernel nodes of the captured iteration graph (prep on the side stream
+// included): what one cudaGraphLaunch puts on the GPU.
+static int count_graph_kernels(cudaGraph_t g) {
+  size_t n = 0;
+  if (!g || cudaGraphGetNodes(g, nullptr, &n) != cudaSuccess) return 0;
+  std::vector<cudaGraphNode_t> nodes(n);
+  if (cudaGraphGetNodes(g, nodes.data(), &n) != cudaSuccess) return 0;
+  int k = 0;
+  for (auto nd : nodes) {
+    cudaGraphNodeType ty;
+    if (cudaGraphNodeGetType(nd, &ty) == cudaSuccess && ty == cudaGraphNodeTypeKernel) ++k;
+  }
+  return k;
+}
+
 // Run every queued model to retirement.  `pool` must already hold the
 // starting factors (per model, per mode, row-major I_n x R_k).
 // Lo-slice fusion (UpdArgs::lo): when the first contraction after mode 0
@@ -1466,6 +1485,7 @@ static int engine_run(Engine* e, double tol, int max_iterations, double sqnorm, 
   if (use_graph) {
     rc = engine_capture(e, stream);
     if (rc) return rc;
+    e->graph_kernels = count_graph_kernels(e->graph);
   }
   // tol <= 0: the iteration count is known, so the graphs go out back to back
   // (no completion polling, no trailing no-op iterations)
@@ -1520,6 +1540,8 @@ static int engine_run(Engine* e, double tol, int max_iterations, double sqnorm, 
   CALS_CHECK(*(volatile int*)e->h_done, kErrInvalid, "engine did not terminate");
   const int plans = ((volatile int*)e->h_done)[1];
   e->last_iterations = plans - 1;
+  // reset + initial plan + move, then one graph per launched iteration
+  e->last_launches = 3 + (use_graph ? launched * e->graph_kernels : 0);
   if (iterations_out) *iterations_out = plans - 1;
   return kOk;
 }
@@ -1730,6 +1752,12 @@ int cals_engine_run(cals_engine* e, double tol, int max_iterations, double sqnor
   }
 #endif
   return rc;
+}
+
+int cals_engine_last_launches(cals_engine* e, long long* launches) {
+  CALS_CHECK(e && launches, kErrInvalid, "null argument");
+  *launches = e->e->last_launches;
+  return kOk;
 }
 
 int cals_engine_pool_download(cals_engine* e, double* host_pool, void* stream) {

@@ -154,6 +154,13 @@ class CalsEngine:
                      ptr(err), ptr(fit), ptr(seq), ptr(secs), ptr(lam), s)
         return EngineResults(pool, status, iters, err, fit, seq, secs, lam)
 
+    def last_launches(self) -> int:
+        """Kernel launches of the last ``run`` (graph kernel nodes x graph
+        launches + the direct ones), counted by the library."""
+        n = C.c_longlong()
+        _native.call("cals_engine_last_launches", self.handle, C.byref(n))
+        return int(n.value)
+
     def pool_download(self, pool_out: np.ndarray, stream=None) -> None:
         """Enqueue the pool's device-to-host copy into ``pool_out`` (page-locked)
         without waiting; synchronise the stream before reading it."""
