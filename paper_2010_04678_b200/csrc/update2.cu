@@ -284,14 +284,29 @@ __device__ __forceinline__ void tile_gram_tc(const double* __restrict__ X, int P
     const int ca = ti * 8 + r_lo, cb = tj * 8 + r_lo;
     const bool va = ca < R, vb = cb < R;
     const int s0 = steps * part / parts, s1 = steps * (part + 1) / parts;
-    double d0 = 0.0, d1 = 0.0;
-    for (int st = s0; st < s1; ++st) {
+    // two independent DMMA chains (even / odd K steps), added at the end:
+    // half the dependent-accumulation latency of one chain
+    double d0 = 0.0, d1 = 0.0, e0 = 0.0, e1 = 0.0;
+    int st = s0;
+    for (; st + 2 <= s1; st += 2) {
+      const int kk = st * 4 + k_lo, kn = kk + 4;
+      const bool vk = kk < cnt, vn = kn < cnt;
+      const double av = (va && vk) ? X[kk * P + ca] : 0.0;
+      const double bv = (vb && vk) ? X[kk * P + cb] : 0.0;
+      const double an = (va && vn) ? X[kn * P + ca] : 0.0;
+      const double bn = (vb && vn) ? X[kn * P + cb] : 0.0;
+      dmma_8x8x4(d0, d1, av, bv);
+      dmma_8x8x4(e0, e1, an, bn);
+    }
+    if (st < s1) {
       const int kk = st * 4 + k_lo;
       const bool vk = kk < cnt;
       const double av = (va && vk) ? X[kk * P + ca] : 0.0;
       const double bv = (vb && vk) ? X[kk * P + cb] : 0.0;
       dmma_8x8x4(d0, d1, av, bv);
     }
+    d0 += e0;
+    d1 += e1;
     if (parts == 1) {
       const int gr = ti * 8 + r_lo, gc = tj * 8 + 2 * k_lo;
       if (gr < R && gc < R) {
