@@ -268,3 +268,28 @@ def test_single_als_raises_on_update_failure(cals):
     with pytest.raises(ValueError):
         cals.run_single_als(t, bad, cals.ConvergenceConfig(tol=0.0, max_iterations=3))
     assert bad.status.value == str(g["single_input_status"])
+
+
+def test_launch_counter_matches_graph(cals):
+    """cals_engine_last_launches: reset + initial plan + move, then the kernel
+    nodes of the captured iteration graph once per driver iteration (tol 0:
+    exactly max_iterations graphs for a batch admitted at once)."""
+    from paper_2010_04678_b200.engine import CalsEngine
+
+    import torch
+
+    t = cals.generate_synthetic((60, 50, 40), 4, 0.1, seed=2)
+    models = cals.build_models(t.dims, [2, 3, 4], 2, seed=3)
+    eng = CalsEngine(t.device(), 18, [m.rank for m in models])
+    pool = torch.from_numpy(eng.pack([m.factors for m in models])).cuda()
+    counts = []
+    for iters in (3, 5):
+        eng.load_pool(pool)
+        assert eng.run(0.0, iters, t.sqnorm) == iters
+        counts.append(eng.last_launches())
+    eng.close()
+    per_iter = (counts[1] - counts[0]) // 2
+    # per iteration: 3 contractions or 2 + a TTV, their reductions / slicing,
+    # 3 prep + 3 solve kernels, plan and move
+    assert 8 <= per_iter <= 24, counts
+    assert counts[0] == 3 + 3 * per_iter and counts[1] == 3 + 5 * per_iter
