@@ -67,11 +67,19 @@ def drive_mode0_sharded(engines, tol: float, max_iterations: int, sqnorm: float,
         e.begin(tol, max_iterations, sqnorm)
     bufs = [e.buffers() for e in engines]
     dims = engines[0].dims
+    # tol <= 0: every admitted model runs exactly max_iterations, so the number
+    # of driver iterations is known from the FIFO admission alone and they are
+    # enqueued back to back (stream-ordered NCCL all-reduces, no per-iteration
+    # host round trip); failures only retire models earlier, which leaves the
+    # remaining iterations no-ops on the device
+    known = fixed_iteration_count(engines[0].ranks, engines[0].r_star,
+                                  max_iterations) if tol <= 0 else 0
     iters = 0
     while True:
-        torch.cuda.current_stream().synchronize()
-        if all(e.done() for e in engines):
-            return iters
+        if known <= 0 or iters >= known:
+            torch.cuda.current_stream().synchronize()
+            if all(e.done() for e in engines):
+                return iters
         for n in range(order):
             for e in engines:
                 e.enqueue_mttkrp(n)
@@ -84,6 +92,40 @@ def drive_mode0_sharded(engines, tol: float, max_iterations: int, sqnorm: float,
         for e in engines:
             e.enqueue_plan()
         iters += 1
+
+
+def fixed_iteration_count(ranks: Sequence[int], capacity: int, max_iterations: int) -> int:
+    """Driver iterations of a run in which every model takes exactly
+    ``max_iterations`` (tol <= 0): the FIFO admission with head-of-line
+    blocking of driver.py:199-208 replayed on the host (as the engine's
+    fixed_iteration_count in csrc/engine.cu).  0 if the queue can block
+    forever (a rank above the capacity)."""
+    active: list[list[int]] = []  # [rank, iterations left]
+    head, width, count = 0, 0, 0
+    ranks = [int(r) for r in ranks]
+
+    def admit():
+        nonlocal head, width
+        while head < len(ranks) and width + ranks[head] <= capacity:
+            active.append([ranks[head], max_iterations])
+            width += ranks[head]
+            head += 1
+
+    admit()
+    while active:
+        count += 1
+        keep = []
+        for a in active:
+            a[1] -= 1
+            if a[1] > 0:
+                keep.append(a)
+            else:
+                width -= a[0]
+        active[:] = keep
+        admit()
+        if not active and head < len(ranks):
+            return 0
+    return count
 
 
 def _allreduce_sum(tensors, group=None) -> None:

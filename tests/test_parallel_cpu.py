@@ -123,3 +123,15 @@ def test_config5_slab_generator_gloo():
     signal = np.einsum("ir,jr,kr->ijk", *fac)
     noise = t1 - signal
     assert abs(np.linalg.norm(noise) / np.linalg.norm(signal) - 0.1) < 1e-9
+
+
+def test_fixed_iteration_count_replays_fifo():
+    """The host replay of the FIFO admission (driver.py:199-208) that lets the
+    sharded driver enqueue tol <= 0 sweeps without per-iteration syncs."""
+    from paper_2010_04678_b200.parallel import fixed_iteration_count as f
+
+    assert f([1, 2, 3], 100, 5) == 5              # all admitted at once
+    assert f([4] * 12, 8, 3) == 18                # waves of two (test_driver.py:77-90 shape)
+    assert f([3, 3, 4], 7, 2) == 4                # head-of-line blocking: 3+3, then 4
+    assert f(list(range(1, 21)) * 5, 1050, 5) == 5
+    assert f([5], 4, 3) == 0                      # never admissible
