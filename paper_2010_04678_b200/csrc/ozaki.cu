@@ -130,6 +130,126 @@ __global__ void oz_slice_rows_kernel(const double* __restrict__ x, long long sm,
   }
 }
 
+// Single-pass version of oz_slice_rows_kernel for views whose 32-row block
+// fits in shared memory (Kp <= kRowsTileMaxKp): the block's 32 rows x Kp
+// values are loaded once into tile[p][33] with every load of a thread in
+// flight (the two-pass kernel reads the tensor twice with a dependent chain
+// of loads per thread and moves ~1.1 TB/s), the row maxima come from the same
+// loads, and the slices are written from the tile.  Same exponents, slices
+// and dynamic-range census as oz_slice_rows_kernel.
+constexpr int kRowsTileMaxKp = 384;
+__global__ void __launch_bounds__(256) oz_slice_rows_tile_kernel(
+    const double* __restrict__ x, long long sm, long long sp, long long sq, int M, int Dp, int Kp,
+    int Dq, uint8_t* __restrict__ xs, int* __restrict__ rex, int* __restrict__ out_of_range) {
+  extern __shared__ double tile[];  // [Kp][33]
+  __shared__ double red[8][33];
+  __shared__ int ex[32];
+  const int q = blockIdx.y, m0 = blockIdx.x * 32;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const double* xq = x + (long long)q * sq;
+  if (sm == 1) {  // m contiguous: lanes along m, warps stride p
+    const int m = m0 + lane;
+    const bool mv = m < M;
+    double mx = 0.0;
+    int p = w;
+    for (; p + 8 * 7 < Kp; p += 8 * 8) {
+      double v[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int pu = p + 8 * u;
+        v[u] = (mv && pu < Dp) ? xq[m + (long long)pu * sp] : 0.0;
+      }
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        mx = fmax(mx, abs_or_inf(v[u]));
+        tile[(p + 8 * u) * 33 + lane] = v[u];
+      }
+    }
+    for (; p < Kp; p += 8) {
+      const double v = (mv && p < Dp) ? xq[m + (long long)p * sp] : 0.0;
+      mx = fmax(mx, abs_or_inf(v));
+      tile[p * 33 + lane] = v;
+    }
+    red[w][lane] = mx;
+    __syncthreads();
+    if (w == 0) {
+      double v = red[0][lane];
+#pragma unroll
+      for (int k = 1; k < 8; ++k) v = fmax(v, red[k][lane]);
+      red[0][lane] = v;
+    }
+  } else {  // p contiguous: lanes along p, warps take rows
+    for (int r = w; r < 32; r += 8) {
+      const int m = m0 + r;
+      const bool mv = m < M;
+      const double* row = xq + (long long)m * sm;
+      double mx = 0.0;
+      int p = lane;
+      for (; p + 32 * 3 < Kp; p += 32 * 4) {
+        double v[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int pu = p + 32 * u;
+          v[u] = (mv && pu < Dp) ? row[(long long)pu * sp] : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          mx = fmax(mx, abs_or_inf(v[u]));
+          tile[(p + 32 * u) * 33 + r] = v[u];
+        }
+      }
+      for (; p < Kp; p += 32) {
+        const double v = (mv && p < Dp) ? row[(long long)p * sp] : 0.0;
+        mx = fmax(mx, abs_or_inf(v));
+        tile[p * 33 + r] = v;
+      }
+#pragma unroll
+      for (int o = 16; o; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+      if (lane == 0) red[0][r] = mx;
+    }
+  }
+  __syncthreads();
+  if (w == 0) {
+    const int e = scale_exp_checked(red[0][lane]);
+    ex[lane] = e;
+    const int m = m0 + lane;
+    if (m < M) {
+      rex[(long long)q * M + m] = e;
+      if (e == kNonFinite || e < -900 || e > 900) atomicOr(out_of_range, 1);
+    }
+  }
+  __syncthreads();
+  const size_t slice_stride = size_t(Dq) * size_t(M) * size_t(Kp);
+  int nz = 0, nsmall = 0;
+  for (int r = w; r < 32; r += 8) {
+    const int m = m0 + r;
+    if (m >= M) continue;
+    const int e = ex[r];
+    const double thr = (e == kNonFinite) ? 0.0 : ldexp(1.0, e - kRangeBits);
+    uint8_t* row = xs + (size_t(q) * M + m) * size_t(Kp);
+    for (int p = lane; p < Kp; p += 32) {
+      const double v = tile[p * 33 + r];
+      const double a = fabs(v);
+      nz += a != 0.0;
+      nsmall += a != 0.0 && a < thr;
+      uint8_t sl[kSlices];
+      slice7(v, e, sl);
+#pragma unroll
+      for (int k = 0; k < kSlices; ++k) row[p + k * slice_stride] = sl[k];
+    }
+  }
+#pragma unroll
+  for (int o = 16; o; o >>= 1) {
+    nz += __shfl_xor_sync(0xffffffffu, nz, o);
+    nsmall += __shfl_xor_sync(0xffffffffu, nsmall, o);
+  }
+  if (lane == 0 && nz > 0) {
+    unsigned long long* census = reinterpret_cast<unsigned long long*>(out_of_range + 2);
+    atomicAdd(census, (unsigned long long)nsmall);
+    atomicAdd(census + 1, (unsigned long long)nz);
+  }
+}
+
 // Lo slices: ls[7][cap_pad][Kp] (column c of lo as a p-contiguous row),
 // cex[c] = scale exponent el of column c.  Block (x, y) = 256 threads for
 // columns 32x..32x+31 and p-chunk y (32 values); the column max is taken
@@ -435,8 +555,27 @@ int ozaki_prepare(Tensor& t, const ModePlan& p, int key, cudaStream_t stream, bo
   CALS_CUDA_TRY(cudaMallocAsync(reinterpret_cast<void**>(&flag), kFlagBytes, stream));
   CALS_CUDA_TRY(cudaMemsetAsync(flag, 0, kFlagBytes, stream));
   dim3 grid((unsigned)((p.M + 31) / 32), (unsigned)p.Dq);
-  oz_slice_rows_kernel<<<grid, 256, 0, stream>>>(t.data, sm, sp, sq, (int)p.M, (int)p.Dp,
-                                                 (int)o.Kp, (int)p.Dq, o.xs, o.rex, flag);
+  static const bool tile_ok = [] {  // CALS_OZ_ROWS_TILE=0: two-pass kernel (A/B)
+    const char* env = getenv("CALS_OZ_ROWS_TILE");
+    return !(env && strcmp(env, "0") == 0);
+  }();
+  if (tile_ok && o.Kp <= kRowsTileMaxKp) {
+    const size_t smem = size_t(o.Kp) * 33 * 8;
+    static std::once_flag once;
+    static cudaError_t attr = cudaSuccess;
+    std::call_once(once, [] {
+      attr = cudaFuncSetAttribute(oz_slice_rows_tile_kernel,
+                                  cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  kRowsTileMaxKp * 33 * 8);
+    });
+    CALS_CUDA_TRY(attr);
+    oz_slice_rows_tile_kernel<<<grid, 256, smem, stream>>>(t.data, sm, sp, sq, (int)p.M,
+                                                           (int)p.Dp, (int)o.Kp, (int)p.Dq, o.xs,
+                                                           o.rex, flag);
+  } else {
+    oz_slice_rows_kernel<<<grid, 256, 0, stream>>>(t.data, sm, sp, sq, (int)p.M, (int)p.Dp,
+                                                   (int)o.Kp, (int)p.Dq, o.xs, o.rex, flag);
+  }
   CALS_CUDA_TRY(cudaGetLastError());
   o.flag = flag;
   if (validate) {  // once per tensor and view
