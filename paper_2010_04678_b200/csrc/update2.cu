@@ -219,6 +219,44 @@ __device__ __forceinline__ void finish_model(const UpdArgs& a, int k, double msq
 // carry unused values.  A fully unrolled per-rank solve is ~R^2 instructions
 // of straight-line code fetched cold by every CTA (ncu: no_instruction was the
 // top stall); this body is ~6 R instructions.
+// One substitution sweep for R <= 16 with the next step's pre-shifted row and
+// reciprocal diagonal loaded while the current step runs (two register
+// buffers, steps taken in pairs): a step then costs one DMUL + one DFMA of
+// latency instead of two dependent shared-memory round trips on top.  The FMA
+// sequence per element is solve_row_exact's.  `dir` +1: forward (k = 0 ..
+// R-1, W = Us), -1: back (k = R-1 .. 0, W = Vs).
+template <int R>
+__device__ __forceinline__ void subst_pipelined(double (&r)[R], double* __restrict__ xs,
+                                                const double* __restrict__ W,
+                                                const double* __restrict__ invd, int dir) {
+  constexpr int RS = R + (R & 1);
+  constexpr int RM = R > 1 ? R - 1 : 1;
+  double ua[RM], ub[RM], da, db;
+  auto load = [&](double (&u)[RM], double& d, int s) {  // s: step index 0 .. R-1
+    const int k = dir > 0 ? s : R - 1 - s;
+    d = invd[k];
+#pragma unroll
+    for (int j = 0; j + 1 < R; ++j) u[j] = W[k * RS + j];
+  };
+  auto step = [&](const double (&u)[RM], double d, int s) {
+    const int k = dir > 0 ? s : R - 1 - s;
+    const double y = r[0] * d;
+    xs[k] = y;
+#pragma unroll
+    for (int j = 0; j + 1 < R; ++j) r[j] = fma(-u[j], y, r[j + 1]);
+  };
+  load(ua, da, 0);
+  int s = 0;
+#pragma unroll 1
+  for (; s + 1 < R; s += 2) {
+    load(ub, db, s + 1);
+    step(ua, da, s);
+    load(ua, da, s + 2 < R ? s + 2 : R - 1);
+    step(ub, db, s + 1);
+  }
+  if (s < R) step(ua, da, s);
+}
+
 template <int R>
 __device__ __forceinline__ void solve_row_exact(double* __restrict__ xs,
                                                 const double* __restrict__ Us,
@@ -228,23 +266,30 @@ __device__ __forceinline__ void solve_row_exact(double* __restrict__ xs,
   double r[R];
 #pragma unroll
   for (int c = 0; c < R; ++c) r[c] = xs[c];
+  if constexpr (R <= 16) {
+    subst_pipelined<R>(r, xs, Us, invd, 1);
+#pragma unroll
+    for (int j = 0; j < R; ++j) r[j] = xs[R - 1 - j];
+    subst_pipelined<R>(r, xs, Vs, invd, -1);
+  } else {
 #pragma unroll 1
-  for (int k = 0; k < R; ++k) {
-    const double yk = r[0] * invd[k];
-    xs[k] = yk;
-    const double* u = Us + k * RS;
+    for (int k = 0; k < R; ++k) {
+      const double yk = r[0] * invd[k];
+      xs[k] = yk;
+      const double* u = Us + k * RS;
 #pragma unroll
-    for (int j = 0; j + 1 < R; ++j) r[j] = fma(-u[j], yk, r[j + 1]);
-  }
+      for (int j = 0; j + 1 < R; ++j) r[j] = fma(-u[j], yk, r[j + 1]);
+    }
 #pragma unroll
-  for (int j = 0; j < R; ++j) r[j] = xs[R - 1 - j];
+    for (int j = 0; j < R; ++j) r[j] = xs[R - 1 - j];
 #pragma unroll 1
-  for (int k = R - 1; k >= 0; --k) {
-    const double xk = r[0] * invd[k];
-    xs[k] = xk;
-    const double* v = Vs + k * RS;
+    for (int k = R - 1; k >= 0; --k) {
+      const double xk = r[0] * invd[k];
+      xs[k] = xk;
+      const double* v = Vs + k * RS;
 #pragma unroll
-    for (int j = 0; j + 1 < R; ++j) r[j] = fma(-v[j], xk, r[j + 1]);
+      for (int j = 0; j + 1 < R; ++j) r[j] = fma(-v[j], xk, r[j + 1]);
+    }
   }
 }
 
@@ -351,12 +396,16 @@ __device__ __forceinline__ void tile_gram_tc(const double* __restrict__ X, int P
 // zeros for p in [Dp, Kp).  A / ld: the factor block -- the solved rows still
 // in shared memory, or (failure / pinv-redo paths) F[n] in global memory
 // (this CTA's own stores, visible after the barrier that precedes the call).
-__device__ __noinline__ void slice_lo_columns(const UpdArgs::LoTarget& tg, int off, int R,
-                                              const double* __restrict__ A, long long ld) {
+// The target's fields come by value: taking the address of the kernel
+// parameter block would make the compiler copy all of it to the stack at
+// every solve CTA's entry.
+__device__ __noinline__ void slice_lo_columns(uint8_t* __restrict__ ls, int* __restrict__ cex,
+                                              int* queue, long long stride, int Kp, int Dp,
+                                              int off, int R, const double* __restrict__ A,
+                                              long long ld) {
   __shared__ int ex_s[32];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int Dp = tg.Dp, Kp = tg.Kp;
-  if (tg.queue && blockIdx.x == 0 && tid == 0) *tg.queue = 0;  // the contraction's unit counter
+  if (queue && blockIdx.x == 0 && tid == 0) *queue = 0;  // the contraction's unit counter
   for (int c = warp; c < R; c += kSolveRows / 32) {
     double mx = 0.0;
 #pragma unroll 4
@@ -366,7 +415,7 @@ __device__ __noinline__ void slice_lo_columns(const UpdArgs::LoTarget& tg, int o
     if (lane == 0) {
       const int e = oz::scale_exp_checked(mx);
       ex_s[c] = e;
-      tg.cex[off + c] = e;
+      cex[off + c] = e;
     }
   }
   __syncthreads();
@@ -385,10 +434,10 @@ __device__ __noinline__ void slice_lo_columns(const UpdArgs::LoTarget& tg, int o
 #pragma unroll
       for (int s = 0; s < oz::kSlices; ++s) w[s] |= uint32_t(sl[s]) << (8 * u);
     }
-    uint8_t* dst = tg.ls + size_t(off + c) * Kp + p0;
+    uint8_t* dst = ls + size_t(off + c) * Kp + p0;
 #pragma unroll
     for (int s = 0; s < oz::kSlices; ++s)
-      *reinterpret_cast<uint32_t*>(dst + size_t(s) * tg.stride) = w[s];
+      *reinterpret_cast<uint32_t*>(dst + size_t(s) * stride) = w[s];
   }
 }
 
@@ -398,9 +447,21 @@ __device__ __forceinline__ void slice_lo_targets(const UpdArgs& a, int n, int of
 #pragma unroll
   for (int t = 0; t < 2; ++t)
     if (a.lo[t].src == n) {
-      slice_lo_columns(a.lo[t], off, R, A, ld);
+      slice_lo_columns(a.lo[t].ls, a.lo[t].cex, a.lo[t].queue, a.lo[t].stride, a.lo[t].Kp,
+                       a.lo[t].Dp, off, R, A, ld);
       if (t == 1 && blockIdx.x == 0 && threadIdx.x == 0) *a.lo_stale = 0;
     }
+}
+
+// arr[n] for a runtime n without indexing the kernel parameter block (a
+// dynamic index makes the compiler copy the array to the stack)
+template <class T>
+__device__ __forceinline__ T param_at(const T (&arr)[kMaxOrder], int n) {
+  T v = arr[0];
+#pragma unroll
+  for (int i = 1; i < kMaxOrder; ++i)
+    if (i == n) v = arr[i];
+  return v;
 }
 
 // Shared-memory layout of upd_solve_kernel<RB> (doubles)
@@ -439,7 +500,8 @@ __global__ void __launch_bounds__(kSolveRows, 2) upd_solve_kernel(UpdArgs a, int
   const long long go = si.w;
   const int pf = a.pflag[k];
   const long long ld = a.ld;
-  const int rows = (int)a.dims[n];
+  const int rows = (int)param_at(a.dims, n);
+  double* const Fn = param_at(a.F, n);
   const int r0 = chunk * kSolveRows;
   const int cnt = min(kSolveRows, rows - r0);
   const int P = fast_pitch(R);
@@ -452,7 +514,7 @@ __global__ void __launch_bounds__(kSolveRows, 2) upd_solve_kernel(UpdArgs a, int
     if (LAST && chunk == 0 && tid == 0) finish_model(a, k, 0.0, 0.0, false);
     if (a.lo[0].src == n || a.lo[1].src == n) {  // the factor stays: its slices still feed
       griddep_wait();                                 // the later contraction
-      slice_lo_targets(a, n, off, R, a.F[n] + off, a.ld);
+      slice_lo_targets(a, n, off, R, Fn + off, a.ld);
     }
     return;
   }
@@ -529,7 +591,7 @@ __global__ void __launch_bounds__(kSolveRows, 2) upd_solve_kernel(UpdArgs a, int
       a.failed[k] = 1;
       if (LAST) finish_model(a, k, 0.0, 0.0, false);
     }
-    slice_lo_targets(a, n, off, R, a.F[n] + off, a.ld);
+    slice_lo_targets(a, n, off, R, Fn + off, a.ld);
     return;
   }
   int sbad = 0;
@@ -547,7 +609,7 @@ __global__ void __launch_bounds__(kSolveRows, 2) upd_solve_kernel(UpdArgs a, int
   // coalesced store of the solved rows (+ the last mode's <A, M> partial)
   double dot = 0.0;
   {
-    double* Ac = a.F[n] + (long long)r0 * ld + off;
+    double* Ac = Fn + (long long)r0 * ld + off;
     const double* Mc = Mb + (long long)r0 * ld;
     int i = tid / R, c = tid - (tid / R) * R;
 #pragma unroll 16
@@ -604,7 +666,7 @@ __global__ void __launch_bounds__(kSolveRows, 2) upd_solve_kernel(UpdArgs a, int
       }
     }
   }
-  double* Afull = a.F[n] + off;
+  double* Afull = Fn + off;
   if (redo) {
     // cho_solve gave a non-finite entry: the whole block again with pinv(H)
     // (als.py:88-96); H from the unchanged Gramians of the other modes
@@ -643,7 +705,7 @@ __global__ void __launch_bounds__(kSolveRows, 2) upd_solve_kernel(UpdArgs a, int
   // nch == 1 for a fusion source (setup_lo_fusion): X holds every solved row
   // unless the pinv redo used it as scratch
   if (redo)
-    slice_lo_targets(a, n, off, R, a.F[n] + off, a.ld);
+    slice_lo_targets(a, n, off, R, Fn + off, a.ld);
   else
     slice_lo_targets(a, n, off, R, X, P);
   if (!LAST) return;
