@@ -1120,8 +1120,10 @@ static long long fixed_iteration_count(const Engine* e, int max_iterations) {
   return graphs;
 }
 
-// M_n -> Mout for the current layout (dimension-tree aware).
-static int enqueue_mode_mttkrp(Engine* e, int n, cudaStream_t stream) {
+// M_n -> Mout for the current layout (dimension-tree aware).  With `defer`, a
+// split-K contraction leaves M_n as partials for the solve kernel instead.
+static int enqueue_mode_mttkrp(Engine* e, int n, cudaStream_t stream,
+                               SplitDefer* defer = nullptr) {
   Tensor& t = *e->t;
   const int N = e->order;
   FactorSet fs{};
@@ -1145,7 +1147,8 @@ static int enqueue_mode_mttkrp(Engine* e, int n, cudaStream_t stream) {
       // the partial Y[i + I0p j] kept for mode 1
       rc = launch_contraction(t, e->tree_plan, 100, F[2], t.dims[2], ld, F[1], ld, 0, wptr, cap,
                               Mo, ld, e->d_ws, e->tree_variant, stream, e->d_partial, ld, t.i0p,
-                              oz_ws, oz_bytes, false, e->lo_carry ? e->h_st.lo_stale : nullptr);
+                              oz_ws, oz_bytes, false, e->lo_carry ? e->h_st.lo_stale : nullptr,
+                              defer);
     } else if (e->tree == kTreeY && n == 1) {
       // M1 = Y x_i A0(new): A2 unchanged since Y was formed
       rc = launch_partial_ttv(e->d_partial, ld, t.i0p, t.dims[1], 0, t.dims[0], F[0], ld, 0,
@@ -1154,7 +1157,7 @@ static int enqueue_mode_mttkrp(Engine* e, int n, cudaStream_t stream) {
       // M1 = sum_k A2[k] (sum_i X[i,:,k] A0(new)[i]); slab products = Z[j + I1 k]
       rc = launch_contraction(t, e->tree_plan, 1, F[0], t.dims[0], ld, F[2], ld, 0, wptr, cap, Mo,
                               ld, e->d_ws, e->tree_variant, stream, e->d_partial, ld, t.dims[1],
-                              oz_ws, oz_bytes, n == e->lo_target);
+                              oz_ws, oz_bytes, n == e->lo_target, nullptr, defer);
     } else if (e->tree == kTreeZ && n == 2) {
       // M2 = Z x_j A1(new): A0 unchanged since Z was formed
       rc = launch_partial_ttv(e->d_partial, ld, t.dims[1], t.dims[2], 0, t.dims[1], F[1], ld, 0,
@@ -1162,7 +1165,7 @@ static int enqueue_mode_mttkrp(Engine* e, int n, cudaStream_t stream) {
     } else {
       rc = launch_mttkrp(t, n, fs, 0, wptr, cap, Mo, ld, e->d_ws, e->ws_bytes, e->variants[n],
                          stream, n == e->lo_target,
-                         (n == 0 && e->lo_carry) ? e->h_st.lo_stale : nullptr);
+                         (n == 0 && e->lo_carry) ? e->h_st.lo_stale : nullptr, defer);
     }
     if (rc) return rc;
   }
@@ -1210,6 +1213,15 @@ bool pdl_enabled() {
   return on;
 }
 
+// CALS_DEFER_REDUCE=0 keeps split_reduce_kernel in front of every solve (A/B)
+static bool defer_reduce_enabled() {
+  static const bool on = [] {
+    const char* v = getenv("CALS_DEFER_REDUCE");
+    return !v || atoi(v) != 0;
+  }();
+  return on;
+}
+
 // Split update of mode n: prep(n) forked onto the side stream before the
 // MTTKRP of mode n is queued (it depends only on what the main stream has
 // done so far), solve(n) after both.
@@ -1219,8 +1231,18 @@ static int enqueue_split_mode(Engine* e, int n, cudaStream_t stream) {
   e->prep_kernel<<<e->max_slots, kPrepThreads, 0, e->side>>>(e->ua, n);
   CALS_CUDA_TRY(cudaGetLastError());
   CALS_CUDA_TRY(cudaEventRecord(e->ev_join[n], e->side));
-  int rc = enqueue_mode_mttkrp(e, n, stream);
+  // non-last modes: the solve sums the split-K partials itself (the last
+  // mode's M also feeds the fit's <A, M>, read after the solve)
+  SplitDefer defer;
+  const bool defer_ok = n < e->order - 1 && defer_reduce_enabled() &&
+                        (long long)e->t->dims[n] * e->ld < (1LL << 31);
+  int rc = enqueue_mode_mttkrp(e, n, stream, defer_ok ? &defer : nullptr);
   if (rc) return rc;
+  UpdArgs ua = e->ua;
+  ua.mpart = defer.part;
+  ua.mpart_stride = defer.stride;
+  ua.mpart_ld = defer.ldp;
+  ua.mS = defer.S;
   CALS_CUDA_TRY(cudaStreamWaitEvent(stream, e->ev_join[n], 0));
   SolveKernel k = n == e->order - 1 ? e->solve_last_kernel : e->solve_kernel;
   // programmatic launch: the solve's prologue (slot, pflag, U) overlaps the
@@ -1235,7 +1257,7 @@ static int enqueue_split_mode(Engine* e, int n, cudaStream_t stream) {
   at[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
   cfg.attrs = at;
   cfg.numAttrs = 1;
-  CALS_CUDA_TRY(cudaLaunchKernelEx(&cfg, k, e->ua, n, e->nch[n]));
+  CALS_CUDA_TRY(cudaLaunchKernelEx(&cfg, k, ua, n, e->nch[n]));
   return kOk;
 }
 

@@ -113,6 +113,27 @@ struct FactorSet {
   long long ld;                  // leading dimension (columns), even
 };
 
+// Split-K partials left for the consumer: with a SplitDefer passed to the
+// launches below, an S > 1 contraction skips its split_reduce_kernel and
+// reports where its partials are (block s, row m, column c at
+// part[s * stride + m * ldp + c]); the consumer sums them in s order, the
+// reduction's own order (the split update's solve kernel, update2.cu).
+// S stays 0 when the contraction wrote `out` itself.
+struct SplitDefer {
+  const double* part = nullptr;
+  long long stride = 0;
+  long long ldp = 0;
+  int S = 0;
+};
+// Only partial sets that stay L2-resident are deferred: the solve kernel's
+// staging re-reads them per model block (c3: 11 x 251 x 300 doubles, 6.6 MB,
+// 4.26k -> 4.32k models/s); c2's 84 MB partial set, mostly evicted by the
+// dimension tree's side output, reduces faster in split_reduce_kernel
+// (28.8k vs 29.1k).
+inline bool split_deferrable(int S, long long M, long long ldp) {
+  return S > 1 && double(S) * double(M) * double(ldp) * 8.0 <= 24.0 * (1 << 20);
+}
+
 // Launch one fused MTTKRP (+ split reduction) on `stream`.  `width` is used
 // when width_ptr is null; otherwise the kernels read the active width from
 // device memory (engine path, graph-capturable).  `cap` bounds the width and
@@ -120,7 +141,8 @@ struct FactorSet {
 int launch_mttkrp(Tensor& t, int mode, const FactorSet& f, int width, const int* width_ptr,
                   long long cap, double* out, long long ldo, double* workspace,
                   size_t workspace_bytes, int variant, cudaStream_t stream,
-                  bool lo_sliced = false, const int* lo_stale = nullptr);
+                  bool lo_sliced = false, const int* lo_stale = nullptr,
+                  SplitDefer* defer = nullptr);
 // The Ozaki workspace launch_mttkrp carves for `mode` out of `workspace`
 // (nullptr when the mode does not run on the INT8 path or it does not fit).
 void* mttkrp_oz_ws(Tensor& t, int mode, long long ld, void* workspace, size_t workspace_bytes);
@@ -137,7 +159,7 @@ int launch_contraction(Tensor& t, const ModePlan& p, int map_key, const double* 
                        double* part, int variant, cudaStream_t stream, double* side = nullptr,
                        long long side_ld = 0, long long side_qstride = 0, void* oz_ws = nullptr,
                        size_t oz_ws_bytes = 0, bool lo_sliced = false,
-                       const int* lo_stale = nullptr);
+                       const int* lo_stale = nullptr, SplitDefer* defer = nullptr);
 
 // Ozaki-sliced INT8 tensor-core contraction (ozaki.cu) ------------------------
 bool ozaki_enabled();                       // CALS_MTTKRP=dmma disables it
@@ -177,7 +199,7 @@ int launch_contraction_ozaki(Tensor& t, const ModePlan& p, int key, const double
                              long long ldo, double* part, void* oz_ws, size_t oz_ws_bytes,
                              cudaStream_t stream, double* side, long long side_ld,
                              long long side_qstride, bool lo_sliced = false,
-                             const int* lo_stale = nullptr);
+                             const int* lo_stale = nullptr, SplitDefer* defer = nullptr);
 
 // out[row][c] = sum over the reduced index of P[a + Da*b][c] * F[idx][c]
 // (reduce_b: rows a < rows_out, sum b < Db with F[b]; else rows b, sum a < La

@@ -484,7 +484,7 @@ size_t mttkrp_workspace_bytes(const Tensor& t, int mode, long long cap) {
 int launch_mttkrp(Tensor& t, int mode, const FactorSet& f, int width, const int* width_ptr,
                   long long cap, double* out, long long ldo, double* workspace,
                   size_t workspace_bytes, int variant, cudaStream_t stream, bool lo_sliced,
-                  const int* lo_stale) {
+                  const int* lo_stale, SplitDefer* defer) {
   CALS_CHECK(mode >= 0 && mode < t.order, kErrInvalid, "mode out of range");
   const ModePlan& p = t.plans[mode];
   CALS_CHECK(f.ld % 2 == 0 && f.ld >= cap, kErrInvalid, "factor leading dimension must be even");
@@ -565,7 +565,7 @@ int launch_mttkrp(Tensor& t, int mode, const FactorSet& f, int width, const int*
   }
   return launch_contraction(t, p, mode, lo, lrows, lo_ld, hi, hi_ld, width, width_ptr, cap, out,
                             ldo, part, variant, stream, nullptr, 0, 0, oz_ws, oz_bytes, lo_sliced,
-                            lo_stale);
+                            lo_stale, defer);
 }
 
 void* mttkrp_oz_ws(Tensor& t, int mode, long long ld, void* workspace, size_t workspace_bytes) {
@@ -586,7 +586,8 @@ int launch_contraction(Tensor& t, const ModePlan& p, int map_key, const double* 
                        int width, const int* width_ptr, long long cap, double* out, long long ldo,
                        double* part, int variant, cudaStream_t stream, double* side,
                        long long side_ld, long long side_qstride, void* oz_ws,
-                       size_t oz_ws_bytes, bool lo_sliced, const int* lo_stale) {
+                       size_t oz_ws_bytes, bool lo_sliced, const int* lo_stale,
+                       SplitDefer* defer) {
   static const bool dbg = getenv("CALS_DEBUG_OZ") != nullptr;
   if (dbg)
     fprintf(stderr, "[oz] contraction key=%d role=%d M=%lld Dp=%lld Dq=%lld S=%d oz_ws=%p elig=%d\n",
@@ -595,7 +596,7 @@ int launch_contraction(Tensor& t, const ModePlan& p, int map_key, const double* 
     const int rc = launch_contraction_ozaki(t, p, map_key, lo, lrows, lo_ld, hi, hi_ld, width,
                                             width_ptr, cap, out, ldo, part, oz_ws, oz_ws_bytes,
                                             stream, side, side_ld, side_qstride, lo_sliced,
-                                            lo_stale);
+                                            lo_stale, defer);
     if (dbg) fprintf(stderr, "[oz]   ozaki rc=%d\n", rc);
     if (rc != kErrUnsupported) return rc;  // unsupported = slices not prepared: DMMA below
   }
@@ -654,7 +655,9 @@ int launch_contraction(Tensor& t, const ModePlan& p, int map_key, const double* 
   dim3 grid((unsigned)std::max<long long>(1, std::min(units, slots)));
   const bool kcontig = p.role == kRoleMiddle || p.role == kRoleLast;
   CALS_CUDA_TRY(ve.launch(grid, mapA, mapB, a, kcontig, stream));
-  if (p.S > 1) {
+  if (defer && split_deferrable(p.S, p.M, lo_ld)) {
+    *defer = SplitDefer{part, a.part_stride, lo_ld, p.S};
+  } else if (p.S > 1) {
     const long long pairs = p.M * ((cap + 1) / 2);
     const int blocks = (int)std::max<long long>(1, std::min<long long>(sms * 8, (pairs + 255) / 256));
     CALS_CUDA_TRY(launch_dep(split_reduce_kernel, dim3(blocks), dim3(256), 0, stream,

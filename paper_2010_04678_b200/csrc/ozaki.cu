@@ -646,7 +646,8 @@ int launch_contraction_ozaki(Tensor& t, const ModePlan& p, int key, const double
                              int width, const int* width_ptr, long long cap, double* out,
                              long long ldo, double* part, void* oz_ws, size_t oz_ws_bytes,
                              cudaStream_t stream, double* side, long long side_ld,
-                             long long side_qstride, bool lo_sliced, const int* lo_stale) {
+                             long long side_qstride, bool lo_sliced, const int* lo_stale,
+                             SplitDefer* defer) {
   OzSlices o;
   {
     std::lock_guard<std::mutex> lk(t.mu);
@@ -771,7 +772,9 @@ int launch_contraction_ozaki(Tensor& t, const ModePlan& p, int key, const double
     CALS_CUDA_TRY(launch_dep(mttkrp_ozaki_kernel<false>, grid, dim3(kThreads), kSmemBytes, stream,
                              o.map, mapL, o.rmap, a));
   CALS_CUDA_TRY(cudaGetLastError());
-  if (p.S > 1) {
+  if (defer && split_deferrable(p.S, p.M, lo_ld)) {
+    *defer = SplitDefer{part, a.part_stride, lo_ld, p.S};
+  } else if (p.S > 1) {
     const long long pairs = p.M * ((cap + 1) / 2);
     const int blocks =
         (int)std::max<long long>(1, std::min<long long>(sms * 8, (pairs + 255) / 256));

@@ -551,7 +551,11 @@ __global__ void __launch_bounds__(kSolveRows, 2) upd_solve_kernel(UpdArgs a, int
   // The reference checks the whole M block before touching the factor
   // (als.py:84-85): every chunk scans all of it (one chunk at <= 256 rows),
   // staging its own rows on the way, so all chunks reach the same verdict.
-  const double* Mb = a.Mout + off;
+  // M_n straight from the contraction's split-K partials (non-last modes,
+  // SplitDefer): summed here in split order instead of by split_reduce_kernel
+  const bool parts = !LAST && a.mS > 1;
+  const double* Mb = (parts ? a.mpart : a.Mout) + off;
+  const long long ldm = parts ? a.mpart_ld : ld;
   int bad = pf == kPrepBadH;
   // everything above came from earlier kernels (plan, prep); M_n is the
   // output of the grid right before this one (programmatic launch)
@@ -559,7 +563,52 @@ __global__ void __launch_bounds__(kSolveRows, 2) upd_solve_kernel(UpdArgs a, int
   // element e = i * R + c of the block walked with stride kSolveRows without
   // integer divisions: (i, c) advance by (dq, dr) per step
   const int dq = kSolveRows / R, dr = kSolveRows - dq * R;
-  {
+  if (parts) {
+    constexpr int B = 8;
+    const int S = a.mS;
+    const long long ps = a.mpart_stride;
+    int i = tid / R, c = tid - (tid / R) * R;
+    while (i < rows) {
+      int eo[B], xi[B];
+      double v[B];
+#pragma unroll
+      for (int u = 0; u < B; ++u) {
+        const bool ok = i < rows;
+        const int il = i - r0;
+        eo[u] = ok ? int((long long)i * ldm + c) : -1;
+        xi[u] = ok && il >= 0 && il < cnt ? il * P + c : -1;
+        v[u] = ok ? Mb[eo[u]] : 0.0;
+        i += dq;
+        c += dr;
+        if (c >= R) {
+          c -= R;
+          ++i;
+        }
+      }
+      // partials 1 .. S-1 added in order (split_reduce_kernel's), four blocks
+      // of loads in flight per round
+      int s = 1;
+      for (; s + 4 <= S; s += 4) {
+        double w[4][B];
+#pragma unroll
+        for (int t = 0; t < 4; ++t)
+#pragma unroll
+          for (int u = 0; u < B; ++u) w[t][u] = eo[u] >= 0 ? Mb[(s + t) * ps + eo[u]] : 0.0;
+#pragma unroll
+        for (int t = 0; t < 4; ++t)
+#pragma unroll
+          for (int u = 0; u < B; ++u) v[u] += w[t][u];
+      }
+      for (; s < S; ++s)
+#pragma unroll
+        for (int u = 0; u < B; ++u) v[u] += eo[u] >= 0 ? Mb[s * ps + eo[u]] : 0.0;
+#pragma unroll
+      for (int u = 0; u < B; ++u) {
+        bad |= !isfinite(v[u]);
+        if (xi[u] >= 0) X[xi[u]] = v[u];
+      }
+    }
+  } else {
     int i = tid / R, c = tid - (tid / R) * R;
     while (i < rows) {
       double v[16];
@@ -675,9 +724,14 @@ __global__ void __launch_bounds__(kSolveRows, 2) upd_solve_kernel(UpdArgs a, int
     block_pinv(U, X, lam, R);
     for (long long e = tid; e < (long long)rows * R; e += kSolveRows) {
       const int i = int(e / R), c = int(e % R);
-      const double* m = Mb + (long long)i * ld;
+      const double* m = Mb + (long long)i * ldm;
       double s = 0.0;
-      for (int b = 0; b < R; ++b) s = fma(m[b], U[b * R + c], s);
+      for (int b = 0; b < R; ++b) {
+        double mb = m[b];
+        if (parts)
+          for (int q = 1; q < a.mS; ++q) mb += m[q * a.mpart_stride + b];
+        s = fma(mb, U[b * R + c], s);
+      }
       Afull[(long long)i * ld + c] = s;
     }
     __syncthreads();

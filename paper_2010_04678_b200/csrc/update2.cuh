@@ -55,6 +55,13 @@ struct UpdArgs {
   double* gpart;           // per model [chunk][R][R] partial Gramians (chunks > 1)
   double* ipart;           // last mode: per model [chunk] partial <A, M>
   const double* Mout;
+  // M_n as split-K partials (SplitDefer, internal.h) instead of Mout: set per
+  // solve launch of a non-last mode whose contraction skipped its reduction
+  // (mS <= 1: read Mout)
+  const double* mpart;
+  long long mpart_stride;
+  long long mpart_ld;
+  int mS;
   double* F[kMaxOrder];
   long long dims[kMaxOrder];
   long long ld;
