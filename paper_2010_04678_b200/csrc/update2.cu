@@ -7,7 +7,7 @@ namespace cals {
 
 #ifdef CALS_SOLVE_PROFILE
 // per (mode, CTA) clock64 stamps of the solve kernel: [0] R, [1..8] phases
-__device__ long long g_solve_prof[8][2048][10];
+__device__ long long g_solve_prof[8][2048][16];
 #define SOLVE_STAMP(i) \
   if (tid == 0 && blockIdx.x < 2048) g_solve_prof[n][blockIdx.x][i] = clock64() - t_entry;
 #else
@@ -560,11 +560,15 @@ __global__ void __launch_bounds__(kSolveRows, 2) upd_solve_kernel(UpdArgs a, int
   // everything above came from earlier kernels (plan, prep); M_n is the
   // output of the grid right before this one (programmatic launch)
   griddep_wait();
+  SOLVE_STAMP(8)
   // element e = i * R + c of the block walked with stride kSolveRows without
   // integer divisions: (i, c) advance by (dq, dr) per step
   const int dq = kSolveRows / R, dr = kSolveRows - dq * R;
   if (parts) {
-    constexpr int B = 8;
+    // B elements per round with up to G partial blocks of each in flight at
+    // once: a c3 block (S = 11) costs one L2 round trip per round instead of
+    // one per group of four partials
+    constexpr int B = 4, G = 10;
     const int S = a.mS;
     const long long ps = a.mpart_stride;
     int i = tid / R, c = tid - (tid / R) * R;
@@ -585,23 +589,21 @@ __global__ void __launch_bounds__(kSolveRows, 2) upd_solve_kernel(UpdArgs a, int
           ++i;
         }
       }
-      // partials 1 .. S-1 added in order (split_reduce_kernel's), four blocks
-      // of loads in flight per round
-      int s = 1;
-      for (; s + 4 <= S; s += 4) {
-        double w[4][B];
+      // partials 1 .. S-1 added in order (split_reduce_kernel's); a lane
+      // past S adds nothing (not even +0.0, which would turn -0.0 into +0.0)
+      for (int s = 1; s < S; s += G) {
+        double w[G][B];
 #pragma unroll
-        for (int t = 0; t < 4; ++t)
+        for (int t = 0; t < G; ++t)
 #pragma unroll
-          for (int u = 0; u < B; ++u) w[t][u] = eo[u] >= 0 ? Mb[(s + t) * ps + eo[u]] : 0.0;
+          for (int u = 0; u < B; ++u)
+            w[t][u] = (s + t < S && eo[u] >= 0) ? Mb[(s + t) * ps + eo[u]] : 0.0;
 #pragma unroll
-        for (int t = 0; t < 4; ++t)
+        for (int t = 0; t < G; ++t)
 #pragma unroll
-          for (int u = 0; u < B; ++u) v[u] += w[t][u];
+          for (int u = 0; u < B; ++u)
+            if (s + t < S) v[u] += w[t][u];
       }
-      for (; s < S; ++s)
-#pragma unroll
-        for (int u = 0; u < B; ++u) v[u] += eo[u] >= 0 ? Mb[s * ps + eo[u]] : 0.0;
 #pragma unroll
       for (int u = 0; u < B; ++u) {
         bad |= !isfinite(v[u]);
@@ -655,6 +657,7 @@ __global__ void __launch_bounds__(kSolveRows, 2) upd_solve_kernel(UpdArgs a, int
     }
   }
   __syncthreads();
+  SOLVE_STAMP(4)
   // coalesced store of the solved rows (+ the last mode's <A, M> partial)
   double dot = 0.0;
   {
@@ -674,7 +677,7 @@ __global__ void __launch_bounds__(kSolveRows, 2) upd_solve_kernel(UpdArgs a, int
       }
     }
   }
-  SOLVE_STAMP(4)
+  SOLVE_STAMP(9)
   // Gramian refresh from the solved rows (driver.py:234)
   tile_gram_tc(X, P, cnt, R, scr, Gs);
   double inner = 0.0;
@@ -762,12 +765,14 @@ __global__ void __launch_bounds__(kSolveRows, 2) upd_solve_kernel(UpdArgs a, int
     slice_lo_targets(a, n, off, R, Fn + off, a.ld);
   else
     slice_lo_targets(a, n, off, R, X, P);
+  SOLVE_STAMP(10)
   if (!LAST) return;
   // fast error (als.py:99-115): sum of the Hadamard of all Gramians, folded
   // ascending -- (G_0 o .. o G_{N-2}) from prep, then o G_{N-1}
   double mpart = 0.0;
   for (int idx = tid; idx < R * R; idx += kSolveRows) mpart += Hs[idx] * Gs[idx];
   const double msq = block_sum(mpart, red);
+  SOLVE_STAMP(11)
   if (tid == 0) finish_model_pre(a, k, msq, inner, din, ls_on);
   SOLVE_STAMP(7)
 }
