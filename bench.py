@@ -330,6 +330,49 @@ def run_reference_arm(args) -> None:
 
 
 # --------------------------------------------------------------- our arm ---
+def secondary_sweep(name: str, stream, flush, warmup: int = 1, steps: int = 3) -> dict:
+    """A second workload timed beside the headline (default N = 1 run only):
+    device-resident sweeps through the same engine path as ``value`` (pool
+    re-loaded every step, L2 flushed between steps, CUDA events on the engine
+    stream).  Reported under ``secondary`` -- not the headline metric."""
+    import torch
+
+    import paper_2010_04678_b200 as cals
+    from paper_2010_04678_b200.engine import CalsEngine
+
+    wl = WORKLOADS[name]
+    t = cals.generate_synthetic(wl["dims"], wl["true_rank"], 0.1, seed=0)
+    models = cals.build_models(wl["dims"], wl["ranks"], wl["per_rank"], seed=1)
+    dev_t = t.device()
+    eng = CalsEngine(dev_t, wl["r_star"], [m.rank for m in models], trace_capacity=64)
+    pool = torch.from_numpy(eng.pack([m.factors for m in models])).cuda()
+    sq = t.sqnorm
+    iters, launches, times = [], [], []
+    for i in range(warmup + steps):
+        flush.fill_(float(i))
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        eng.load_pool(pool)
+        iters.append(eng.run(wl["tol"], wl["iters"], sq))
+        b.record(stream)
+        launches.append(eng.last_launches())
+        torch.cuda.synchronize()
+        if i >= warmup:
+            times.append(a.elapsed_time(b))
+    res = eng.results(with_pool=False)
+    eng.close()
+    t.release_device()
+    ms = float(np.mean(times))
+    return {"metric": _metric(name), "value": len(models) / (ms * 1e-3), "unit": "models/s",
+            "ms_per_step": ms, "steps": steps, "warmup": warmup,
+            "driver_iterations_per_step": float(np.mean(iters[warmup:])),
+            "gpu_launches_per_step": float(np.mean(launches[warmup:])),
+            "statuses": {str(k): int(v) for k, v in zip(*np.unique(res.status,
+                                                                  return_counts=True))},
+            "timing": "device-resident, CUDA events on the engine stream, L2 flushed between "
+                      "steps; config " + wl["desc"]}
+
+
 def main_gpu(args) -> None:
     import ctypes as C
 
@@ -543,9 +586,11 @@ def main_gpu(args) -> None:
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_sample(name, os.cpu_count() or 1,
                                           steps=1 if wl["shard"] or wl["tol"] > 0 else 2)
+    eng.close()
+    if world == 1 and name == "c2" and args.config is None:
+        line["secondary"] = {"c3": secondary_sweep("c3", stream, flush)}
     if rank == 0:
         print(json.dumps(line), flush=True)
-    eng.close()
     if world > 1:
         dist.destroy_process_group()
 
