@@ -187,6 +187,7 @@ def _run_fused(t: DenseTensor, queue: list[Model], cfg: ConvergenceConfig, r_sta
         eng.prepare()  # tensor slicing overlaps the host packing below
         eng.set_line_search(bool(ls is not None and ls.enabled), None if ls is None else ls.alpha)
         eng.set_nonneg(nonneg)
+        t2p = time.perf_counter()
         eng.load_pool(eng.pack([m.factors for m in queue], out=eng.staging()))
         t3 = time.perf_counter()
         sqnorm = t.device_sqnorm()  # waits for both uploads
@@ -224,7 +225,8 @@ def _run_fused(t: DenseTensor, queue: list[Model], cfg: ConvergenceConfig, r_sta
         warnings.warn("active-set search hit its iteration cap", NonConvergedNnlsWarning,
                       stacklevel=3)
     t5 = time.perf_counter()
-    prof.update(tensor_upload_s=t1 - t0, engine_create_s=t2 - t1, pool_upload_s=t3 - t2,
+    prof.update(tensor_upload_s=t1 - t0, engine_create_s=t2 - t1, prepare_s=t2p - t2,
+                pool_upload_s=t3 - t2p,
                 upload_wait_s=tic - t3, device_loop_s=t4 - tic, results_download_s=t5 - t4)
     if not label_per_model:
         for m in queue:
