@@ -975,6 +975,10 @@ static int engine_create(Tensor* t, int capacity, int n_models, const int* ranks
   // split update: kernel-parameter block (constant bank) of device pointers
   ua.st = e->d_st;
   ua.n_active = &e->d_st->n_active;
+  ua.rev = [] {
+    const char* v = getenv("CALS_SOLVE_REV");
+    return !v || atoi(v) != 0;
+  }() ? 1 : 0;
   ua.slot_info = h.slot_info;
   ua.failed = h.failed;
   ua.fresh = h.fresh;

@@ -491,11 +491,17 @@ __global__ void __launch_bounds__(kSolveRows, 2) upd_solve_kernel(UpdArgs a, int
 #ifdef CALS_SOLVE_PROFILE
   const long long t_entry = clock64();
 #endif
-  const int slot = blockIdx.x / nch;
-  const int chunk = blockIdx.x - slot * nch;
+  const int sb = blockIdx.x / nch;
+  const int chunk = blockIdx.x - sb * nch;
   const int na = *a.n_active;
+  if (sb >= na) return;
+  // CTA order: with rev, the last registry slot first.  The block scheduler
+  // gives the first ~148 CTAs an SM of their own and doubles up the rest;
+  // queues built in rank order (build_models) put the widest models last,
+  // and their chains are the kernel's critical path.  Results do not depend
+  // on which CTA solves a model.
+  const int slot = a.rev ? na - 1 - sb : sb;
   const int4 si = a.slot_info[slot];
-  if (slot >= na) return;
   const int k = si.x, R = si.y, off = si.z;
   const long long go = si.w;
   const int pf = a.pflag[k];

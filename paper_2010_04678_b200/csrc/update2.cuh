@@ -84,6 +84,7 @@ struct UpdArgs {
     int src;
   } lo[2];
   int* lo_stale;
+  int rev;  // solve CTAs take the active slots last-first (upd_solve_kernel)
 };
 
 // Shared memory of upd_solve_kernel<RB> (SolveSmem in update2.cu):
