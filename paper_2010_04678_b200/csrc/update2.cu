@@ -235,8 +235,15 @@ __device__ __forceinline__ void subst_pipelined(double (&r)[R], double* __restri
   auto load = [&](double (&u)[RM], double& d, int s) {  // s: step index 0 .. R-1
     const int k = dir > 0 ? s : R - 1 - s;
     d = invd[k];
+    // 16-byte loads (rows of RS doubles, RS even, 16-byte aligned): half the
+    // shared-memory instructions of the step, which all warps issue
+    const double2* w2 = reinterpret_cast<const double2*>(W + k * RS);
 #pragma unroll
-    for (int j = 0; j + 1 < R; ++j) u[j] = W[k * RS + j];
+    for (int j = 0; j + 1 < R; j += 2) {
+      const double2 p = w2[j >> 1];
+      u[j] = p.x;
+      if (j + 1 < RM) u[j + 1] = p.y;
+    }
   };
   auto step = [&](const double (&u)[RM], double d, int s) {
     const int k = dir > 0 ? s : R - 1 - s;
@@ -276,9 +283,13 @@ __device__ __forceinline__ void solve_row_exact(double* __restrict__ xs,
     for (int k = 0; k < R; ++k) {
       const double yk = r[0] * invd[k];
       xs[k] = yk;
-      const double* u = Us + k * RS;
+      const double2* u = reinterpret_cast<const double2*>(Us + k * RS);  // 16-byte loads
 #pragma unroll
-      for (int j = 0; j + 1 < R; ++j) r[j] = fma(-u[j], yk, r[j + 1]);
+      for (int j = 0; j + 1 < R; j += 2) {
+        const double2 p = u[j >> 1];
+        r[j] = fma(-p.x, yk, r[j + 1]);
+        if (j + 2 < R) r[j + 1] = fma(-p.y, yk, r[j + 2]);
+      }
     }
 #pragma unroll
     for (int j = 0; j < R; ++j) r[j] = xs[R - 1 - j];
@@ -286,9 +297,13 @@ __device__ __forceinline__ void solve_row_exact(double* __restrict__ xs,
     for (int k = R - 1; k >= 0; --k) {
       const double xk = r[0] * invd[k];
       xs[k] = xk;
-      const double* v = Vs + k * RS;
+      const double2* v = reinterpret_cast<const double2*>(Vs + k * RS);
 #pragma unroll
-      for (int j = 0; j + 1 < R; ++j) r[j] = fma(-v[j], xk, r[j + 1]);
+      for (int j = 0; j + 1 < R; j += 2) {
+        const double2 p = v[j >> 1];
+        r[j] = fma(-p.x, xk, r[j + 1]);
+        if (j + 2 < R) r[j + 1] = fma(-p.y, xk, r[j + 2]);
+      }
     }
   }
 }
