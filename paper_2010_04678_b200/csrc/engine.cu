@@ -799,6 +799,7 @@ static int setup_tree(Engine* e) {
   }
   e->ws_bytes = std::max(e->ws_bytes, tree_ws_offset(p, e->ld) + ozaki_ws_bytes(p, e->ld) + 256);
   CALS_CUDA_TRY(cudaMalloc(&e->d_partial, bytes));
+  poison_alloc(e->d_partial, bytes);
   e->tree_variant = choose_variant(p.M, e->capacity, p.S);
   e->tree = choice;
   return kOk;
@@ -964,6 +965,7 @@ static int engine_create(Tensor* t, int capacity, int n_models, const int* ranks
   size_t total = 0;
   for (auto& it : items) total = align_up(total, 256) + it.bytes;
   CALS_CUDA_TRY(cudaMalloc(&e->d_block, total));
+  poison_alloc(e->d_block, total);
   CALS_CUDA_TRY(cudaMemset(e->d_block, 0, total));
   size_t off = 0;
   for (auto& it : items) {
@@ -972,6 +974,7 @@ static int engine_create(Tensor* t, int capacity, int n_models, const int* ranks
     off += it.bytes;
   }
   CALS_CUDA_TRY(cudaMalloc(&e->d_st, sizeof(EngState)));
+  poison_alloc(e->d_st, sizeof(EngState));
   // split update: kernel-parameter block (constant bank) of device pointers
   ua.st = e->d_st;
   ua.n_active = &e->d_st->n_active;
@@ -1042,6 +1045,7 @@ static int engine_create(Tensor* t, int capacity, int n_models, const int* ranks
   int rc = setup_tree(e.get());
   if (rc) return rc;
   CALS_CUDA_TRY(cudaMalloc(&e->d_ws, e->ws_bytes));
+  poison_alloc(e->d_ws, e->ws_bytes);
   *out = e.release();
   return kOk;
 }
@@ -1305,6 +1309,7 @@ static int engine_set_nonneg(Engine* e, int enabled) {
       const size_t b_state = align_up(size_t(std::max<long long>(at, 1)) * 4, 256);
       const size_t b_off = align_up(offs.size() * 8, 256);
       CALS_CUDA_TRY(cudaMalloc(&e->d_nnls, b_state + b_off + nm * 4));
+      poison_alloc(e->d_nnls, b_state + b_off + nm * 4);
       CALS_CUDA_TRY(cudaMemset(e->d_nnls, 0, b_state + b_off + nm * 4));
       h.nnls_state = static_cast<unsigned*>(e->d_nnls);
       h.nnls_off = reinterpret_cast<long long*>(static_cast<char*>(e->d_nnls) + b_state);
@@ -1346,6 +1351,7 @@ static int engine_set_line_search(Engine* e, int enabled, double alpha) {
     items.push_back({(void**)&h.e_tmp, nm * 8});
     for (auto& it : items) total = align_up(total, 256) + it.second;
     CALS_CUDA_TRY(cudaMalloc(&e->d_ls, total));
+    poison_alloc(e->d_ls, total);
     CALS_CUDA_TRY(cudaMemset(e->d_ls, 0, total));
     size_t off = 0;
     for (auto& it : items) {

@@ -15,6 +15,26 @@
 
 #include "common.cuh"
 
+#include <cstdlib>
+
+namespace cals {
+// Debug aid (CALS_POISON=1): every workspace allocation is filled with 0xFF
+// bytes (NaN doubles, -1 ints) so a kernel that reads memory nobody wrote
+// shows up as a changed result instead of depending on what the allocator
+// handed back.
+inline bool poison_enabled() {
+  static const bool on = [] {
+    const char* v = getenv("CALS_POISON");
+    return v && atoi(v) != 0;
+  }();
+  return on;
+}
+inline void poison_alloc(void* p, size_t bytes, cudaStream_t s = nullptr, bool async = false) {
+  if (!poison_enabled() || !p || !bytes) return;
+  if (async) cudaMemsetAsync(p, 0xFF, bytes, s); else cudaMemset(p, 0xFF, bytes);
+}
+}  // namespace cals
+
 namespace cals {
 
 constexpr int kMaxOrder = 8;

@@ -251,6 +251,7 @@ int tensor_create(int order, const int64_t* dims, const double* host, const doub
       }
     });
     CALS_CUDA_TRY(cudaMallocAsync(&t->data, bytes, stream));
+    poison_alloc(t->data, bytes, stream, true);
     t->owned = true;
     if (host) {
       if (t->i0p == dims[0]) {  // one linear DMA (full PCIe rate from pinned memory)

@@ -549,7 +549,9 @@ int ozaki_prepare(Tensor& t, const ModePlan& p, int key, cudaStream_t stream, bo
     if (xs_bytes > total / 3) return kOk;
   }
   CALS_CUDA_TRY(cudaMallocAsync(reinterpret_cast<void**>(&o.xs), xs_bytes, stream));
+  poison_alloc(o.xs, xs_bytes, stream, true);
   CALS_CUDA_TRY(cudaMallocAsync(reinterpret_cast<void**>(&o.rex), size_t(p.Dq) * p.M * 4, stream));
+  poison_alloc(o.rex, size_t(p.Dq) * p.M * 4, stream, true);
   int* flag = nullptr;
   // [0] out-of-range / non-finite flag, [2..5] two u64 census counters
   CALS_CUDA_TRY(cudaMallocAsync(reinterpret_cast<void**>(&flag), kFlagBytes, stream));
