@@ -1245,6 +1245,16 @@ static int enqueue_split_mode(Engine* e, int n, cudaStream_t stream) {
   SplitDefer defer;
   const bool defer_ok = n < e->order - 1 && defer_reduce_enabled() &&
                         (long long)e->t->dims[n] * e->ld < (1LL << 31);
+  // the solve of mode n writes its fused Lo-slice targets while other CTAs
+  // of the same launch still stage M_n from the partials: never defer into
+  // a partial set that shares bytes with a target
+  for (int t = 0; t < 2; ++t) {
+    const UpdArgs::LoTarget& tg = e->ua.lo[t];
+    if (tg.src != n) continue;
+    defer.add_avoid(tg.ls, size_t(7) * size_t(tg.stride));  // 7 Ozaki slices (oz::kSlices)
+    defer.add_avoid(tg.cex, size_t(e->capacity + 256) * sizeof(int));
+    defer.add_avoid(tg.queue, sizeof(int));
+  }
   int rc = enqueue_mode_mttkrp(e, n, stream, defer_ok ? &defer : nullptr);
   if (rc) return rc;
   UpdArgs ua = e->ua;

@@ -144,6 +144,28 @@ struct SplitDefer {
   long long stride = 0;
   long long ldp = 0;
   int S = 0;
+  // input: byte ranges the consumer WRITES while other CTAs of it still read
+  // the partials (the solve's fused Lo-slice targets live in the same
+  // workspace).  A partial set overlapping one of them is reduced by
+  // split_reduce_kernel instead of being deferred.
+  static constexpr int kMaxAvoid = 6;
+  const void* avoid[kMaxAvoid] = {};
+  size_t avoid_bytes[kMaxAvoid] = {};
+  int n_avoid = 0;
+  void add_avoid(const void* p, size_t bytes) {
+    if (p && bytes && n_avoid < kMaxAvoid) {
+      avoid[n_avoid] = p;
+      avoid_bytes[n_avoid++] = bytes;
+    }
+  }
+  bool overlaps(const void* p, size_t bytes) const {
+    const char* a0 = static_cast<const char*>(p);
+    for (int i = 0; i < n_avoid; ++i) {
+      const char* b0 = static_cast<const char*>(avoid[i]);
+      if (a0 < b0 + avoid_bytes[i] && b0 < a0 + bytes) return true;
+    }
+    return false;
+  }
 };
 // Only partial sets that stay L2-resident are deferred: the solve kernel's
 // staging re-reads them per model block (c3: 11 x 251 x 300 doubles, 6.6 MB,

@@ -656,7 +656,8 @@ int launch_contraction(Tensor& t, const ModePlan& p, int map_key, const double* 
   dim3 grid((unsigned)std::max<long long>(1, std::min(units, slots)));
   const bool kcontig = p.role == kRoleMiddle || p.role == kRoleLast;
   CALS_CUDA_TRY(ve.launch(grid, mapA, mapB, a, kcontig, stream));
-  if (defer && split_deferrable(p.S, p.M, lo_ld)) {
+  if (defer && split_deferrable(p.S, p.M, lo_ld) &&
+      !defer->overlaps(part, size_t(p.S) * size_t(a.part_stride) * 8)) {
     *defer = SplitDefer{part, a.part_stride, lo_ld, p.S};
   } else if (p.S > 1) {
     const long long pairs = p.M * ((cap + 1) / 2);

@@ -774,7 +774,8 @@ int launch_contraction_ozaki(Tensor& t, const ModePlan& p, int key, const double
     CALS_CUDA_TRY(launch_dep(mttkrp_ozaki_kernel<false>, grid, dim3(kThreads), kSmemBytes, stream,
                              o.map, mapL, o.rmap, a));
   CALS_CUDA_TRY(cudaGetLastError());
-  if (defer && split_deferrable(p.S, p.M, lo_ld)) {
+  if (defer && split_deferrable(p.S, p.M, lo_ld) &&
+      !defer->overlaps(part, size_t(p.S) * size_t(a.part_stride) * 8)) {
     *defer = SplitDefer{part, a.part_stride, lo_ld, p.S};
   } else if (p.S > 1) {
     const long long pairs = p.M * ((cap + 1) / 2);

@@ -12,11 +12,17 @@ import paper_2010_04678_b200 as cals  # noqa: E402
 from oracle import cals_oracle as O  # noqa: E402
 
 reps = int(sys.argv[1]) if len(sys.argv) > 1 else 8
+mix = len(sys.argv) > 2 and sys.argv[2] == "mix"  # other workloads between the repetitions
 dims, data = O.generate_synthetic((250, 251, 21), 10, 0.1, seed=0)
 models = O.build_models(dims, [2, 4, 6, 8, 10], 2, seed=1)
 t = cals.DenseTensor(dims, data)
 base = None
+other = cals.generate_synthetic((60, 50, 40), 4, 0.1, seed=5)
 for i in range(reps):
+    if mix and i:
+        om = cals.build_models(other.dims, [1, 2, 3, 4, 5], 2 + i % 3, seed=i)
+        cals.run(other, om, cals.ConvergenceConfig(tol=1e-5, max_iterations=20 + i),
+                 r_star=9 + i % 5)
     ms = [cals.Model(id=m, rank=r, factors=[f.copy() for f in fac]) for m, r, fac in models]
     out = cals.run(t, ms, cals.ConvergenceConfig(tol=1e-6, max_iterations=300), r_star=30)
     sig = ([m.id for m in out], [m.iterations_done for m in out], [m.fit for m in out],
