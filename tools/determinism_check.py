@@ -37,6 +37,8 @@ for i in range(reps):
     if not same:
         print("   order/iters:", list(zip(sig[0], sig[1])))
         print("   fit diffs:", [a - b for a, b in zip(sig[2], base[2])])
+if "nooracle" in sys.argv:
+    sys.exit(0)
 r1 = O.run_cals(data, dims, models, 1e-6, 300, 30)
 r2 = O.run_cals(data, dims, models, 1e-6, 300, 30)
 print("oracle:", [(r.id, r.iterations) for r in r1])
