@@ -720,6 +720,9 @@ struct Engine {
   // iteration graph x graph launches + the kernels launched directly
   int graph_kernels = 0;
   long long last_launches = 0;
+  // byte offset of the dimension-tree contraction's workspace in d_ws: past
+  // every plain plan's (setup_tree)
+  size_t tree_base = 0;
 };
 
 static size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
@@ -742,6 +745,8 @@ static cudaError_t raise_smem_limit(const void* func, size_t bytes) {
 
 // the tree contraction's split partials sit at the start of the engine
 // workspace, its Ozaki Lo slices after them
+static char* tree_ws(Engine* e) { return reinterpret_cast<char*>(e->d_ws) + e->tree_base; }
+
 static size_t tree_ws_offset(const ModePlan& p, long long ld) {
   return align_up(size_t(p.S) * size_t(p.M) * size_t(ld) * 8, 256);
 }
@@ -797,7 +802,12 @@ static int setup_tree(Engine* e) {
   } else {
     p = t.plans[1];  // MIDDLE: slab product over q = k is Z[j, k, :]
   }
-  e->ws_bytes = std::max(e->ws_bytes, tree_ws_offset(p, e->ld) + ozaki_ws_bytes(p, e->ld) + 256);
+  // the tree contraction's workspace (its split-K partials, then its Ozaki
+  // region) sits past every plain plan's: a deferred partial set of one
+  // contraction never shares bytes with the Lo-slice region a solve writes
+  // for another (SplitDefer::avoid would otherwise keep it undeferred)
+  e->tree_base = align_up(e->ws_bytes, 256);
+  e->ws_bytes = e->tree_base + tree_ws_offset(p, e->ld) + ozaki_ws_bytes(p, e->ld) + 256;
   CALS_CUDA_TRY(cudaMalloc(&e->d_partial, bytes));
   poison_alloc(e->d_partial, bytes);
   e->tree_variant = choose_variant(p.M, e->capacity, p.S);
@@ -1147,7 +1157,7 @@ static int enqueue_mode_mttkrp(Engine* e, int n, cudaStream_t stream,
   size_t oz_bytes = 0;
   if (e->tree != kTreeNone) {
     oz_bytes = ozaki_ws_bytes(e->tree_plan, ld);
-    oz_ws = reinterpret_cast<char*>(e->d_ws) + tree_ws_offset(e->tree_plan, ld);
+    oz_ws = tree_ws(e) + tree_ws_offset(e->tree_plan, ld);
   }
   {
     int rc = kOk;
@@ -1155,7 +1165,7 @@ static int enqueue_mode_mttkrp(Engine* e, int n, cudaStream_t stream,
       // M0 = sum_j A1[j] (sum_k X[:,j,k] A2[k]); the inner slab products are
       // the partial Y[i + I0p j] kept for mode 1
       rc = launch_contraction(t, e->tree_plan, 100, F[2], t.dims[2], ld, F[1], ld, 0, wptr, cap,
-                              Mo, ld, e->d_ws, e->tree_variant, stream, e->d_partial, ld, t.i0p,
+                              Mo, ld, reinterpret_cast<double*>(tree_ws(e)), e->tree_variant, stream, e->d_partial, ld, t.i0p,
                               oz_ws, oz_bytes, false, e->lo_carry ? e->h_st.lo_stale : nullptr,
                               defer);
     } else if (e->tree == kTreeY && n == 1) {
@@ -1165,7 +1175,7 @@ static int enqueue_mode_mttkrp(Engine* e, int n, cudaStream_t stream,
     } else if (e->tree == kTreeZ && n == 1) {
       // M1 = sum_k A2[k] (sum_i X[i,:,k] A0(new)[i]); slab products = Z[j + I1 k]
       rc = launch_contraction(t, e->tree_plan, 1, F[0], t.dims[0], ld, F[2], ld, 0, wptr, cap, Mo,
-                              ld, e->d_ws, e->tree_variant, stream, e->d_partial, ld, t.dims[1],
+                              ld, reinterpret_cast<double*>(tree_ws(e)), e->tree_variant, stream, e->d_partial, ld, t.dims[1],
                               oz_ws, oz_bytes, n == e->lo_target, nullptr, defer);
     } else if (e->tree == kTreeZ && n == 2) {
       // M2 = Z x_j A1(new): A0 unchanged since Z was formed
@@ -1474,7 +1484,7 @@ static void setup_lo_fusion(Engine* e) {
       void* ws;
       if (e->tree == kTreeZ && n == 1) {  // Z = X x_1 A0(new): Lo = F[0]
         p = &e->tree_plan;
-        ws = reinterpret_cast<char*>(e->d_ws) + tree_ws_offset(e->tree_plan, e->ld);
+        ws = tree_ws(e) + tree_ws_offset(e->tree_plan, e->ld);
       } else {
         p = &t.plans[n];
         if (!p->lo_direct() || p->lo_modes[0] != 0) break;
@@ -1499,7 +1509,7 @@ static void setup_lo_fusion(Engine* e) {
       p = &e->tree_plan;
       key = 100;
       src = 2;
-      ws = reinterpret_cast<char*>(e->d_ws) + tree_ws_offset(e->tree_plan, e->ld);
+      ws = tree_ws(e) + tree_ws_offset(e->tree_plan, e->ld);
     } else if (e->tree == kTreeZ && t.plans[0].lo_direct()) {  // mode 0 plain, mode 2 a TTV
       p = &t.plans[0];
       key = 0;
